@@ -1,0 +1,420 @@
+/*
+ * oracle.c — the CPU ORACLE for arXiv 2005.10494's Monte-Carlo design objective.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path (paper_2005_10494_b200/,
+ * include/, the CUDA library) may include, link or call this file.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg use it.
+ * It shares no code, header, table or constant generator with the CUDA path.
+ *
+ * Plain, single-threaded, fp64, written to be checked against PAPER.md by eye.
+ * Citations: P:n = /root/reference/PAPER.md line n (not available at run time;
+ * the citations are for the reader).  Readings of the paper are listed in DESIGN.md §3.
+ *
+ * What it computes, step by step (DESIGN.md §2 gives the contract both sides follow):
+ *   Formula 1 (A.1 P:417-424)  Sigma0[k][l] = sqrt(r_l/r_k), k<l
+ *   Formula 10              Delta ~ N(theta, Sigma_p), Sigma_p = diag(sigma) Sigma0 diag(sigma)
+ *   Formula 3                 X | Delta ~ N(c*Delta, Sigma0), c_i = sqrt(r_i I3)
+ *   Formula 4/5   P(alpha) = 1 - E_Delta[ Phi_Sigma0(z - c*Delta) ]
+ *   Formula 6/7             inner indicator  1[ exists i: X_i > z_i - c_i Delta_i ]  (IND)
+ *   Genz separation of variables        one-sample unbiased estimate of Phi_Sigma0 (COND; reading R6)
+ *   Formula 2                 FWER = 1 - Phi_Sigma0(z_1..z_n)
+ *   Sec. 2.3                    m^(n-1) alpha grid, alpha_n solved, N3 random valid points
+ *
+ * Parity unpinned: none (every function has a pin in tests/test_oracle_*.py).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_MAXN 10
+
+/* ------------------------------------------------------------------------- */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as easy
+ * as 1, 2, 3", SC'11).  Pinned by the Random123 known-answer vectors in
+ * tests/golden/philox4x32_10_kat.txt.  Reading R9: the paper's
+ * Algorithms 1-2 are missing images, so the generator is ours.   */
+void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Word w of design d's stream: block q = w/4 with counter
+ * (q_lo, q_hi, d, 0) and key (seed_lo, seed_hi); the word is lane w mod 4.   */
+uint32_t or_word(uint64_t seed, uint32_t design, uint64_t w)
+{
+    uint64_t q = w / 4;
+    uint32_t ctr[4] = { (uint32_t)q, (uint32_t)(q >> 32), design, 0u };
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint32_t out[4];
+    or_philox4x32_10(ctr, key, out);
+    return out[w % 4];
+}
+
+/* Uniforms from the low 23 bits k of a word.                */
+static double u_radius(uint32_t w) { return 1.0 - (double)(w & 0x7FFFFFu) / 8388608.0; }   /* (0,1] */
+static double u_angle(uint32_t w)  { return (double)(w & 0x7FFFFFu) / 8388608.0; }         /* [0,1) */
+static double u_open(uint32_t w)   { return ((double)(w & 0x7FFFFFu) + 0.5) / 8388608.0; } /* (0,1) */
+
+/* ------------------------------------------------------------------------- */
+/* Standard normal CDF and quantile.                                          */
+double or_Phi(double x) { return 0.5 * erfc(-x / sqrt(2.0)); }
+
+/* Wichura, "Algorithm AS 241: The percentage points of the normal
+ * distribution", Applied Statistics 37 (1988) 477-484 (PPND16).  Pinned
+ * against scipy.special.ndtri in tests/test_oracle_math.py.                  */
+double or_Phi_inv(double p)
+{
+    if (p <= 0.0) return -INFINITY;
+    if (p >= 1.0) return INFINITY;
+    double q = p - 0.5, r, val;
+    if (fabs(q) <= 0.425) {
+        r = 0.180625 - q * q;
+        val = q * (((((((2.5090809287301226727e+3 * r + 3.3430575583588128105e+4) * r
+                        + 6.7265770927008700853e+4) * r + 4.5921953931549871457e+4) * r
+                        + 1.3731693765509461125e+4) * r + 1.9715909503065514427e+3) * r
+                        + 1.3314166789178437745e+2) * r + 3.3871328727963666080e+0)
+                / (((((((5.2264952788528545610e+3 * r + 2.8729085735721942674e+4) * r
+                        + 3.9307895800092710610e+4) * r + 2.1213794301586595867e+4) * r
+                        + 5.3941960214247511077e+3) * r + 6.8718700749205790830e+2) * r
+                        + 4.2313330701600911252e+1) * r + 1.0);
+        return val;
+    }
+    r = (q < 0.0) ? p : 1.0 - p;
+    r = sqrt(-log(r));
+    if (r <= 5.0) {
+        r -= 1.6;
+        val = (((((((7.74545014278341407640e-4 * r + 2.27238449892691845833e-2) * r
+                    + 2.41780725177450611770e-1) * r + 1.27045825245236838258e+0) * r
+                    + 3.64784832476320460504e+0) * r + 5.76949722146069140550e+0) * r
+                    + 4.63033784615654529590e+0) * r + 1.42343711074968357734e+0)
+            / (((((((1.05075007164441684324e-9 * r + 5.47593808499534494600e-4) * r
+                    + 1.51986665636164571966e-2) * r + 1.48103976427480074590e-1) * r
+                    + 6.89767334985100004550e-1) * r + 1.67638483018380384940e+0) * r
+                    + 2.05319162663775882187e+0) * r + 1.0);
+    } else {
+        r -= 5.0;
+        val = (((((((2.01033439929228813265e-7 * r + 2.71155556874348757815e-5) * r
+                    + 1.24266094738807843860e-3) * r + 2.65321895265761230930e-2) * r
+                    + 2.96560571828504891230e-1) * r + 1.78482653991729133580e+0) * r
+                    + 5.46378491116411436990e+0) * r + 6.65790464350110377720e+0)
+            / (((((((2.04426310338993978564e-15 * r + 1.42151175831644588870e-7) * r
+                    + 1.84631831751005468180e-5) * r + 7.86869131145613259100e-4) * r
+                    + 1.48753612908506148525e-2) * r + 1.36929880922735805310e-1) * r
+                    + 5.99832206555887937690e-1) * r + 1.0);
+    }
+    return (q < 0.0) ? -val : val;
+}
+
+/* Threshold Z_{1-alpha}; alpha = 0 means "test never rejects" -> +inf (reading R13). */
+double or_threshold(double alpha)
+{
+    if (alpha <= 0.0) return INFINITY;
+    return or_Phi_inv(1.0 - alpha);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Dense linear algebra: textbook Cholesky A = L L^T (row-major n x n).
+ * Returns 0 on success, (k+1) if the k-th pivot is not positive.            */
+int or_cholesky(int n, const double *A, double *L)
+{
+    memset(L, 0, sizeof(double) * n * n);
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j <= i; ++j) {
+            double s = A[i * n + j];
+            for (int k = 0; k < j; ++k) s -= L[i * n + k] * L[j * n + k];
+            if (i == j) {
+                if (!(s > 0.0)) return i + 1;
+                L[i * n + i] = sqrt(s);
+            } else {
+                L[i * n + j] = s / L[j * n + j];
+            }
+        }
+    }
+    return 0;
+}
+
+/* Formula 1 / Appendix A.1: Sigma0[k][l] = sqrt(r_l / r_k) for k <= l (r_1 = 1). */
+void or_null_corr(int n, const double *r, double *S)
+{
+    for (int k = 0; k < n; ++k)
+        for (int l = 0; l < n; ++l) {
+            int a = k < l ? k : l, b = k < l ? l : k;
+            S[k * n + l] = sqrt(r[b] / r[a]);
+        }
+}
+
+/* ------------------------------------------------------------------------- */
+/* One draw (design d, sample s) of the per-draw utility.
+ *   n, p   populations, prior dimensions (p = n for the Formula-10 prior)
+ *   r[n]   subpopulation fractions; i3 information units
+ *   theta[p], Lp[p*p] prior mean and lower Cholesky factor (row-major) of Sigma_p
+ *   z[n]   thresholds Z_{1-alpha_i} (+inf allowed)
+ *   est    0 = COND (Genz SOV), 1 = IND (Formula 6/7 indicator)
+ * Outputs (may be NULL): eps[p] prior normals, delta[n], b[n], w_null[n] (IND) .
+ * Returns u in [0,1]: the success probability (COND) or indicator (IND).    */
+int or_words_per_draw(int n, int p, int est)
+{
+    if (est == 0) return 2 * ((p + 1) / 2) + (n - 1);
+    return 2 * ((p + n + 1) / 2);
+}
+
+double or_draw(int n, int p, const double *r, double i3, const double *theta, const double *Lp,
+               const double *z, int est, uint64_t seed, uint32_t design, uint64_t s,
+               double *eps_out, double *delta_out, double *b_out, double *wnull_out)
+{
+    const int U = or_words_per_draw(n, p, est);
+    const uint64_t w0 = s * (uint64_t)U;
+    const int nnorm = (est == 0) ? p : p + n;
+    double normals[2 * OR_MAXN + 2];
+    /* Box-Muller: pair j uses words 2j (radius) and 2j+1 (angle). */
+    for (int j = 0; 2 * j < nnorm; ++j) {
+        double R = sqrt(-2.0 * log(u_radius(or_word(seed, design, w0 + 2 * j))));
+        double a = 2.0 * M_PI * u_angle(or_word(seed, design, w0 + 2 * j + 1));
+        normals[2 * j] = R * cos(a);
+        normals[2 * j + 1] = R * sin(a);
+    }
+    /* Formula 10: Delta = theta + Lp * eps. */
+    double delta[OR_MAXN], b[OR_MAXN];
+    for (int i = 0; i < n; ++i) {
+        double acc = theta[i];
+        for (int k = 0; k <= i && k < p; ++k) acc += Lp[i * p + k] * normals[k];
+        delta[i] = acc;
+    }
+    /* Formulas 3-5: thresholds of Phi_Sigma0 are z_i - sqrt(r_i I3) Delta_i. */
+    for (int i = 0; i < n; ++i) b[i] = z[i] - sqrt(r[i] * i3) * delta[i];
+    if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
+    if (delta_out) for (int i = 0; i < n; ++i) delta_out[i] = delta[i];
+    if (b_out) for (int i = 0; i < n; ++i) b_out[i] = b[i];
+
+    double S0[OR_MAXN * OR_MAXN], L0[OR_MAXN * OR_MAXN];
+    or_null_corr(n, r, S0);
+    if (or_cholesky(n, S0, L0) != 0) return NAN;
+
+    if (est == 1) {
+        /* Formula 6/7 with one independent null draw per sample (reading R1):
+         * x = L0 W ~ N(0, Sigma0); success iff some X_i exceeds its threshold.   */
+        int reject = 0;
+        for (int i = 0; i < n; ++i) {
+            double x = 0.0;
+            for (int k = 0; k <= i; ++k) x += L0[i * n + k] * normals[p + k];
+            if (wnull_out) wnull_out[i] = x;
+            if (x > b[i]) reject = 1;
+        }
+        return reject ? 1.0 : 0.0;
+    }
+    /* COND: Genz separation of variables in natural order.  With Y iid N(0,1),
+     * X = L0 Y; e_i = P(X_i <= b_i | y_1..y_{i-1}) = Phi((b_i - sum_{j<i} L0_ij y_j)/L0_ii),
+     * y_i = Phi^{-1}(v_i e_i).  prod_i e_i is an unbiased estimate of Phi_Sigma0(b).   */
+    const int vbase = 2 * ((p + 1) / 2);
+    double y[OR_MAXN], prod = 1.0;
+    for (int i = 0; i < n; ++i) {
+        double m = 0.0;
+        for (int j = 0; j < i; ++j) m += L0[i * n + j] * y[j];
+        double e = or_Phi((b[i] - m) / L0[i * n + i]);
+        prod *= e;
+        if (prod == 0.0) break;                       /* u = 1 exactly; later y are irrelevant */
+        if (i + 1 < n) {
+            double v = u_open(or_word(seed, design, w0 + vbase + i));
+            y[i] = or_Phi_inv(v * e);
+        }
+    }
+    return 1.0 - prod;
+}
+
+/* Per-design sums over samples [s0, s0+count): each draw's u
+ * and u^2 are rounded (half-to-even) to the 2^-23 grid and added as integers.  */
+void or_design_sums(int n, int p, const double *r, double i3, const double *theta, const double *Lp,
+                    const double *z, int est, uint64_t seed, uint32_t design,
+                    uint64_t s0, uint64_t count, int64_t *sums)
+{
+    int64_t a1 = 0, a2 = 0;
+    for (uint64_t s = s0; s < s0 + count; ++s) {
+        double u = or_draw(n, p, r, i3, theta, Lp, z, est, seed, design, s, NULL, NULL, NULL, NULL);
+        a1 += (int64_t)nearbyint(ldexp(u, 23));
+        a2 += (int64_t)nearbyint(ldexp(u * u, 23));
+    }
+    sums[0] += a1;
+    sums[1] += a2;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Gauss-Legendre rule on [-1,1] by Newton iteration on P_G (textbook).       */
+static void gauss_legendre(int G, double *x, double *w)
+{
+    for (int i = 0; i < G; ++i) {
+        double t = cos(M_PI * (i + 0.75) / (G + 0.5)), dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = t;
+            for (int k = 2; k <= G; ++k) { double p2 = ((2.0 * k - 1.0) * t * p1 - (k - 1.0) * p0) / k; p0 = p1; p1 = p2; }
+            dp = G * (t * p1 - p0) / (t * t - 1.0);
+            double dt = p1 / dp;
+            t -= dt;
+            if (fabs(dt) < 1e-16) break;
+        }
+        x[i] = t;
+        w[i] = 2.0 / ((1.0 - t * t) * dp * dp);
+    }
+}
+
+/* Composite Gauss-Legendre nodes on [a, b] with panels no wider than h. */
+static int panel_nodes(double a, double b, double h, double *xs, double *ws, int cap)
+{
+    enum { G = 10 };
+    double gx[G], gw[G];
+    gauss_legendre(G, gx, gw);
+    if (!(b > a)) return 0;
+    int P = (int)ceil((b - a) / h);
+    if (P * G > cap) P = cap / G;
+    double len = (b - a) / P;
+    int m = 0;
+    for (int k = 0; k < P; ++k) {
+        double lo = a + k * len;
+        for (int g = 0; g < G; ++g) {
+            xs[m] = lo + 0.5 * len * (gx[g] + 1.0);
+            ws[m] = 0.5 * len * gw[g];
+            ++m;
+        }
+    }
+    return m;
+}
+
+static double phi_pdf(double x) { return exp(-0.5 * x * x) / sqrt(2.0 * M_PI); }
+
+/* Phi_Sigma0(b) = P(X_i <= b_i, i = 1..n) for the Formula-1 correlation.
+ * Appendix A.1 makes corr(X_k, X_l) = sqrt(r_l/r_k) = prod_{j=k}^{l-1} rho_j with
+ * rho_j = sqrt(r_{j+1}/r_j): X is a Gaussian Markov chain X_{j+1} = rho_j X_j + s_j W,
+ * s_j = sqrt(1 - rho_j^2).  The orthant is the chain's iterated integral
+ *   Phi = int_{-inf}^{b_1} phi(x_1) h_1(x_1) dx_1,
+ *   h_k(x) = int_{-inf}^{b_{k+1}} phi((y - rho_k x)/s_k)/s_k h_{k+1}(y) dy,
+ *   h_{n-1}(x) = Phi((b_n - rho_{n-1} x)/s_{n-1}),
+ * evaluated with composite Gauss-Legendre on [-9, min(b_k, 9)] (mass outside < 1e-18). */
+double or_mvn_orthant(int n, const double *r, const double *b)
+{
+    if (n == 1) return or_Phi(b[0]);
+    double rho[OR_MAXN], sd[OR_MAXN], smin = 1.0;
+    for (int k = 0; k + 1 < n; ++k) {
+        rho[k] = sqrt(r[k + 1] / r[k]);
+        sd[k] = sqrt(1.0 - r[k + 1] / r[k]);
+        if (sd[k] < smin) smin = sd[k];
+    }
+    const double LO = -9.0, HI = 9.0;
+    double h = 0.5 * smin; if (h > 0.5) h = 0.5;
+    enum { CAP = 8000 };
+    static double xs[OR_MAXN][CAP], ws[OR_MAXN][CAP], hv[OR_MAXN][CAP];
+    int m[OR_MAXN];
+    for (int k = 0; k + 1 < n; ++k) {
+        double up = b[k] < HI ? b[k] : HI;
+        if (up <= LO) return 0.0;
+        m[k] = panel_nodes(LO, up, h, xs[k], ws[k], CAP);
+    }
+    /* level n-1 (0-based n-2): closed-form last conditional */
+    int L = n - 2;
+    for (int j = 0; j < m[L]; ++j)
+        hv[L][j] = isinf(b[n - 1]) ? 1.0 : or_Phi((b[n - 1] - rho[L] * xs[L][j]) / sd[L]);
+    for (int k = L - 1; k >= 0; --k) {
+        for (int i = 0; i < m[k]; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < m[k + 1]; ++j)
+                acc += ws[k + 1][j] * phi_pdf((xs[k + 1][j] - rho[k] * xs[k][i]) / sd[k]) / sd[k] * hv[k + 1][j];
+            hv[k][i] = acc;
+        }
+    }
+    double acc = 0.0;
+    for (int j = 0; j < m[0]; ++j) acc += ws[0][j] * phi_pdf(xs[0][j]) * hv[0][j];
+    return acc;
+}
+
+/* Formula 2: FWER(alpha) = 1 - Phi_Sigma0(Z_{1-alpha_1}, ..., Z_{1-alpha_n}). */
+double or_fwer(int n, const double *r, const double *alpha)
+{
+    double z[OR_MAXN];
+    for (int i = 0; i < n; ++i) z[i] = or_threshold(alpha[i]);
+    return 1.0 - or_mvn_orthant(n, r, z);
+}
+
+/* Sec. 2.1 re-parametrisation: solve FWER(alpha_1..alpha_{n-1}, a) = alpha0 for
+ * a in [0, alpha0] by bisection (FWER is increasing in a).  Returns 1 and writes *an
+ * when feasible; 0 when FWER(.., 0) > alpha0 (reading R12: the point is invalid). */
+int or_solve_alpha_n(int n, const double *r, double alpha0, const double *partial, double tol, double *an)
+{
+    double a[OR_MAXN];
+    for (int i = 0; i + 1 < n; ++i) a[i] = partial[i];
+    if (n == 1) { *an = alpha0; return 1; }
+    a[n - 1] = 0.0;
+    /* FWER(.., 0) decides feasibility up to quadrature rounding: |err| < 1e-12 (R12). */
+    double f0 = or_fwer(n, r, a) - alpha0;
+    if (f0 > 1e-12) return 0;
+    if (f0 >= -1e-12) { *an = 0.0; return 1; }
+    double lo = 0.0, hi = alpha0;
+    while (hi - lo > tol) {
+        double mid = 0.5 * (lo + hi);
+        a[n - 1] = mid;
+        if (or_fwer(n, r, a) - alpha0 > 0.0) hi = mid; else lo = mid;
+    }
+    *an = 0.5 * (lo + hi);
+    return 1;
+}
+
+/* Sec. 2.3: the m^(n-1) half-offset grid alpha_j = (k_j + 1/2) alpha0 / m on
+ * (0, alpha0)^(n-1) (reading R8/R10), first coordinate slowest.  Writes every grid
+ * point's feasibility flag and solved alpha_n.  Returns the number of grid points.   */
+int64_t or_alpha_grid(int n, const double *r, double alpha0, int m, double tol,
+                      double *alpha_out /* [m^(n-1) * n] */, uint8_t *valid_out)
+{
+    int64_t G = 1;
+    for (int i = 0; i + 1 < n; ++i) G *= m;
+    for (int64_t g = 0; g < G; ++g) {
+        double part[OR_MAXN];
+        int64_t rem = g;
+        for (int i = n - 2; i >= 0; --i) { part[i] = ((double)(rem % m) + 0.5) * alpha0 / m; rem /= m; }
+        double an = 0.0;
+        int ok = or_solve_alpha_n(n, r, alpha0, part, tol, &an);
+        for (int i = 0; i + 1 < n; ++i) alpha_out[g * n + i] = part[i];
+        alpha_out[g * n + n - 1] = ok ? an : NAN;
+        valid_out[g] = (uint8_t)ok;
+    }
+    return G;
+}
+
+/* Seeded N3-subset of V valid points (reading R11): partial Fisher-Yates over
+ * idx = [0, V) with word i of the Philox stream key (seed_lo ^ 0x00C0FFEE, seed_hi),
+ * counter (i/4, 0, 0, 0xC0FFEE): j = i + floor(word * (V - i) / 2^32).  The chosen
+ * indices are returned in ascending order.                                    */
+static int cmp_i64(const void *a, const void *b)
+{
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return (x > y) - (x < y);
+}
+
+void or_subset(int64_t V, int64_t n3, uint64_t seed, int64_t *out)
+{
+    int64_t *idx = (int64_t *)malloc(sizeof(int64_t) * (V > 0 ? V : 1));
+    for (int64_t i = 0; i < V; ++i) idx[i] = i;
+    uint32_t key[2] = { (uint32_t)seed ^ 0x00C0FFEEu, (uint32_t)(seed >> 32) };
+    for (int64_t i = 0; i < n3; ++i) {
+        uint32_t ctr[4] = { (uint32_t)(i / 4), (uint32_t)((uint64_t)i >> 34), 0u, 0x00C0FFEEu };
+        uint32_t o[4];
+        or_philox4x32_10(ctr, key, o);
+        uint64_t word = o[i % 4];
+        int64_t j = i + (int64_t)((word * (uint64_t)(V - i)) >> 32);
+        int64_t t = idx[i]; idx[i] = idx[j]; idx[j] = t;
+    }
+    for (int64_t i = 0; i < n3; ++i) out[i] = idx[i];
+    qsort(out, (size_t)n3, sizeof(int64_t), cmp_i64);
+    free(idx);
+}

@@ -1,0 +1,395 @@
+"""CPU ORACLE for arXiv 2005.10494 — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` leg may import this module.  The product package
+``paper_2005_10494_b200`` never imports it and shares no code with it.
+
+Plain fp64: the Monte-Carlo estimator, Philox, the MVN orthant and the alpha grid
+are in ``oracle.c`` (ctypes); problem setup (Formula 10, Eq. 9), the closed-form
+assurance, thin-plate-spline smoothing with GCV and the argmax are numpy below.
+``P:n`` cites /root/reference/PAPER.md line n; ``R#`` are the readings in DESIGN.md §3.
+
+Parity unpinned: none — every function is pinned in tests/test_oracle_*.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+MAXN = 10
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (plain -O2, no fast-math: IEEE fp64 semantics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-D_DEFAULT_SOURCE", "-fPIC", "-shared",
+                               "-fno-fast-math", "-ffp-contract=off", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        d, i32, i64, u32, u64 = ctypes.c_double, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
+        P = ctypes.POINTER
+        L.or_philox4x32_10.argtypes = [P(u32), P(u32), P(u32)]
+        L.or_word.argtypes = [u64, u32, u64]
+        L.or_word.restype = u32
+        L.or_Phi.argtypes = [d]; L.or_Phi.restype = d
+        L.or_Phi_inv.argtypes = [d]; L.or_Phi_inv.restype = d
+        L.or_threshold.argtypes = [d]; L.or_threshold.restype = d
+        L.or_cholesky.argtypes = [i32, P(d), P(d)]; L.or_cholesky.restype = i32
+        L.or_null_corr.argtypes = [i32, P(d), P(d)]
+        L.or_words_per_draw.argtypes = [i32, i32, i32]; L.or_words_per_draw.restype = i32
+        L.or_draw.argtypes = [i32, i32, P(d), d, P(d), P(d), P(d), i32, u64, u32, u64,
+                              P(d), P(d), P(d), P(d)]
+        L.or_draw.restype = d
+        L.or_design_sums.argtypes = [i32, i32, P(d), d, P(d), P(d), P(d), i32, u64, u32, u64, u64, P(i64)]
+        L.or_mvn_orthant.argtypes = [i32, P(d), P(d)]; L.or_mvn_orthant.restype = d
+        L.or_fwer.argtypes = [i32, P(d), P(d)]; L.or_fwer.restype = d
+        L.or_solve_alpha_n.argtypes = [i32, P(d), d, P(d), d, P(d)]; L.or_solve_alpha_n.restype = i32
+        L.or_alpha_grid.argtypes = [i32, P(d), d, i32, d, P(d), P(ctypes.c_uint8)]
+        L.or_alpha_grid.restype = i64
+        L.or_subset.argtypes = [i64, i64, u64, P(i64)]
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+# --------------------------------------------------------------------------------------
+# Random stream
+
+def philox4x32_10(ctr, key):
+    c = (ctypes.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(x) & 0xFFFFFFFF for x in key])
+    o = (ctypes.c_uint32 * 4)()
+    lib().or_philox4x32_10(c, k, o)
+    return [int(x) for x in o]
+
+
+def word(seed: int, design: int, w: int) -> int:
+    return int(lib().or_word(seed, design, w))
+
+
+def words_per_draw(n: int, p: int, est: int) -> int:
+    return int(lib().or_words_per_draw(n, p, est))
+
+
+# --------------------------------------------------------------------------------------
+# Normal CDF / quantile
+
+def Phi(x: float) -> float:
+    return float(lib().or_Phi(float(x)))
+
+
+def Phi_inv(p: float) -> float:
+    return float(lib().or_Phi_inv(float(p)))
+
+
+def threshold(alpha: float) -> float:
+    """Z_{1-alpha}; alpha = 0 -> +inf (reading R13)."""
+    return float(lib().or_threshold(float(alpha)))
+
+
+# --------------------------------------------------------------------------------------
+# Problem model (Sec. 2.1, Sec. 3)
+
+def information_units(alpha: float = 0.025, beta: float = 0.1, delta: float = 0.2) -> float:
+    """Eq. 9: I3 = (Z_{1-alpha} + Z_{1-beta})^2 / log(1 - Delta)^2."""
+    za, zb = Phi_inv(1.0 - alpha), Phi_inv(1.0 - beta)
+    return (za + zb) ** 2 / np.log(1.0 - delta) ** 2
+
+
+def null_corr(r) -> np.ndarray:
+    """Formula 1 / A.1: Sigma0[k][l] = sqrt(r_l / r_k), k <= l."""
+    r = np.asarray(r, dtype=np.float64)
+    n = len(r)
+    S = np.empty((n, n))
+    for k in range(n):
+        for l in range(n):
+            a, b = min(k, l), max(k, l)
+            S[k, l] = np.sqrt(r[b] / r[a])
+    return S
+
+
+def cholesky(A) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    L = np.zeros((n, n))
+    rc = lib().or_cholesky(n, _dp(A), L.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if rc != 0:
+        raise np.linalg.LinAlgError(f"matrix not positive definite at pivot {rc - 1}")
+    return L
+
+
+@dataclass
+class Problem:
+    """One fixed-r design problem: r, I3, alpha0 and the effect prior f(Delta)."""
+    r: np.ndarray
+    i3: float
+    alpha0: float
+    theta: np.ndarray
+    prior_cov: np.ndarray
+    Lp: np.ndarray = field(init=False)
+
+    def __post_init__(self):
+        self.r = np.asarray(self.r, dtype=np.float64)
+        self.theta = np.asarray(self.theta, dtype=np.float64)
+        self.prior_cov = np.asarray(self.prior_cov, dtype=np.float64)
+        self.Lp = cholesky(self.prior_cov) if np.any(self.prior_cov) else np.zeros_like(self.prior_cov)
+
+    @property
+    def n(self) -> int:
+        return len(self.r)
+
+    @property
+    def c(self) -> np.ndarray:
+        """Formula 3: mean of X_i is sqrt(r_i I3) Delta_i."""
+        return np.sqrt(self.r * self.i3)
+
+
+def formula10_problem(r, delta0, i3: float, alpha0: float = 0.025, sigma=None) -> Problem:
+    """Formula 10: theta_i = -log(1 - Delta0_i), sigma_i = 1/sqrt(80 r_i / 4),
+    Sigma_p[k][l] = sqrt(r_l / r_k) sigma_k sigma_l (readings R4, R5)."""
+    r = np.asarray(r, dtype=np.float64)
+    theta = -np.log(1.0 - np.asarray(delta0, dtype=np.float64))
+    if sigma is None:
+        sigma = 1.0 / np.sqrt(80.0 * r / 4.0)
+    sigma = np.asarray(sigma, dtype=np.float64) * np.ones_like(r)
+    cov = null_corr(r) * np.outer(sigma, sigma)
+    return Problem(r=r, i3=float(i3), alpha0=float(alpha0), theta=theta, prior_cov=cov)
+
+
+def point_mass_problem(r, theta, i3: float, alpha0: float = 0.025) -> Problem:
+    r = np.asarray(r, dtype=np.float64)
+    return Problem(r=r, i3=float(i3), alpha0=float(alpha0), theta=np.asarray(theta, dtype=np.float64),
+                   prior_cov=np.zeros((len(r), len(r))))
+
+
+# --------------------------------------------------------------------------------------
+# Monte-Carlo estimator (Formulas 5-7 with the readings of DESIGN.md §2)
+
+EST_COND, EST_IND = 0, 1
+
+
+def thresholds(alpha) -> np.ndarray:
+    return np.array([threshold(a) for a in np.asarray(alpha, dtype=np.float64)])
+
+
+def draw(prob: Problem, alpha, est: int, seed: int, design: int, s: int) -> dict:
+    """One draw: returns the prior normals, Delta, b and u (for per-draw parity)."""
+    n = prob.n
+    p = n
+    z = thresholds(alpha)
+    eps, delta, b, wn = np.zeros(p), np.zeros(n), np.zeros(n), np.zeros(n)
+    P = ctypes.POINTER(ctypes.c_double)
+    u = lib().or_draw(n, p, _dp(prob.r), prob.i3, _dp(prob.theta), _dp(prob.Lp), _dp(z), est,
+                      seed, design, s, eps.ctypes.data_as(P), delta.ctypes.data_as(P),
+                      b.ctypes.data_as(P), wn.ctypes.data_as(P))
+    return {"u": float(u), "eps": eps, "delta": delta, "b": b, "xnull": wn}
+
+
+def design_sums(prob: Problem, alpha, est: int, seed: int, design: int, s0: int, count: int) -> np.ndarray:
+    """Integer sums (sum q(u), sum q(u^2)) over samples [s0, s0+count), q = round(2^23 x)."""
+    n = prob.n
+    z = thresholds(alpha)
+    sums = np.zeros(2, dtype=np.int64)
+    lib().or_design_sums(n, n, _dp(prob.r), prob.i3, _dp(prob.theta), _dp(prob.Lp), _dp(z), est, seed,
+                         design, s0, count, sums.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    return sums
+
+
+def finalize(sums, N: int):
+    """Formula 5/7 estimate and per-draw variance (A.2): mean = S1/(N 2^23),
+    var = (S2/(N 2^23) - mean^2) N/(N-1), SE = sqrt(var/N)."""
+    S = np.asarray(sums, dtype=np.float64).reshape(-1, 2)
+    mean = S[:, 0] / (N * 2.0 ** 23)
+    m2 = S[:, 1] / (N * 2.0 ** 23)
+    var = (m2 - mean * mean) * N / max(N - 1, 1)
+    return mean, var
+
+
+# --------------------------------------------------------------------------------------
+# Exact references (pins for the estimand)
+
+def mvn_orthant(r, b) -> float:
+    """Phi_Sigma0(b) by the Markov-chain iterated integral (A.1 => Markov; see oracle.c)."""
+    r = np.asarray(r, dtype=np.float64)
+    return float(lib().or_mvn_orthant(len(r), _dp(r), _dp(np.asarray(b, dtype=np.float64))))
+
+
+def fwer(r, alpha) -> float:
+    """Formula 2."""
+    r = np.asarray(r, dtype=np.float64)
+    return float(lib().or_fwer(len(r), _dp(r), _dp(np.asarray(alpha, dtype=np.float64))))
+
+
+def solve_alpha_n(r, alpha0: float, partial, tol: float = 1e-13):
+    r = np.asarray(r, dtype=np.float64)
+    out = ctypes.c_double(0.0)
+    ok = lib().or_solve_alpha_n(len(r), _dp(r), float(alpha0), _dp(np.asarray(partial, dtype=np.float64)),
+                                tol, ctypes.byref(out))
+    return float(out.value) if ok else None
+
+
+def assurance_gaussian(prob: Problem, alpha) -> float:
+    """Exact P(alpha) for a Gaussian prior (Formula 4): X = c*Delta + E with E ~ N(0, Sigma0)
+    independent of Delta ~ N(theta, Sigma_p), so X ~ N(c*theta, V), V = Sigma0 + C Sigma_p C, and
+    P = 1 - P(X <= z).  Standardising, the bound is (z_i - c_i theta_i)/sqrt(V_ii) under the
+    correlation R = V / sqrt(diag V diag V).  For Formula 10, C Sigma_p C = (I3/20) Sigma0, so R =
+    Sigma0 (SURVEY finding 1).  R must have the Formula-1 (Markov) form for some r'; else raise."""
+    z = thresholds(alpha)
+    c = prob.c
+    V = null_corr(prob.r) + np.outer(c, c) * prob.prior_cov
+    sd = np.sqrt(np.diag(V))
+    R = V / np.outer(sd, sd)
+    # R must be a Formula-1 correlation for some r' (then the orthant is Markov).
+    rp = R[0, :] ** 2
+    if not np.allclose(null_corr(rp), R, rtol=0, atol=1e-12):
+        raise ValueError("prior does not preserve the nested (Markov) correlation")
+    b = (z - c * prob.theta) / sd
+    return 1.0 - mvn_orthant(rp, b)
+
+
+# --------------------------------------------------------------------------------------
+# Candidate designs (Sec. 2.3)
+
+def alpha_grid(r, alpha0: float, m: int, tol: float = 1e-13):
+    """All m^(n-1) half-offset grid points: (alpha[G, n], valid[G])."""
+    r = np.asarray(r, dtype=np.float64)
+    n = len(r)
+    G = m ** (n - 1)
+    A = np.zeros((G, n))
+    V = np.zeros(G, dtype=np.uint8)
+    lib().or_alpha_grid(n, _dp(r), float(alpha0), int(m), tol, A.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                        V.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+    return A, V.astype(bool)
+
+
+def subset(V: int, n3: int, seed: int) -> np.ndarray:
+    out = np.zeros(max(n3, 1), dtype=np.int64)
+    lib().or_subset(int(V), int(n3), int(seed), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    return out[:n3]
+
+
+def candidates(r, alpha0: float, m: int, n3: int, seed: int, tol: float = 1e-13) -> np.ndarray:
+    """Valid grid points in grid order; if 0 < n3 < #valid, the seeded N3 subset (R11)."""
+    A, ok = alpha_grid(r, alpha0, m, tol)
+    valid = A[ok]
+    if n3 <= 0 or n3 >= len(valid):
+        if n3 > len(valid):
+            raise ValueError(f"only {len(valid)} valid candidates < N3={n3}")
+        return valid
+    return valid[subset(len(valid), n3, seed)]
+
+
+# --------------------------------------------------------------------------------------
+# Thin-plate-spline smoothing (Sec. 2.3; readings R16)
+
+def tps_phi(rho: np.ndarray, d: int) -> np.ndarray:
+    """Polyharmonic TPS kernel for penalty order m = 2 (Green's function of the m=2 penalty up to a
+    positive factor): d=1 -> rho^3, d=2 -> rho^2 log rho, d=3 -> -rho."""
+    rho = np.asarray(rho, dtype=np.float64)
+    if d == 2:
+        with np.errstate(divide="ignore", invalid="ignore"):
+            out = np.where(rho > 0, rho * rho * np.log(np.where(rho > 0, rho, 1.0)), 0.0)
+        return out
+    if d == 1:
+        return rho ** 3
+    if d == 3:
+        return -rho
+    raise ValueError(f"TPS dimension d={d} not supported (1..3)")
+
+
+def tps_system(x: np.ndarray):
+    x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    if x.shape[0] == 1 and x.shape[1] > 1 and x.ndim == 2:
+        pass
+    N, d = x.shape
+    D = np.sqrt(((x[:, None, :] - x[None, :, :]) ** 2).sum(-1))
+    K = tps_phi(D, d)
+    T = np.hstack([np.ones((N, 1)), x])
+    return K, T
+
+
+def tps_fit(x, y, lam: float):
+    """Solve [K + N lam I, T; T^T, 0][w; beta] = [y; 0] (the penalised least-squares TPS,
+    1/N sum (y - f)^2 + lam J(f)).  Returns (fitted values, w, beta)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    y = np.asarray(y, dtype=np.float64)
+    K, T = tps_system(x)
+    N, k = T.shape
+    M = np.zeros((N + k, N + k))
+    M[:N, :N] = K + N * lam * np.eye(N)
+    M[:N, N:] = T
+    M[N:, :N] = T.T
+    sol = np.linalg.solve(M, np.concatenate([y, np.zeros(k)]))
+    w, beta = sol[:N], sol[N:]
+    fitted = K @ w + T @ beta
+    return fitted, w, beta
+
+
+def tps_influence(x, lam: float) -> np.ndarray:
+    """Influence matrix A(lam): fitted = A y (solve with identity right-hand sides)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    K, T = tps_system(x)
+    N, k = T.shape
+    M = np.zeros((N + k, N + k))
+    M[:N, :N] = K + N * lam * np.eye(N)
+    M[:N, N:] = T
+    M[N:, :N] = T.T
+    rhs = np.zeros((N + k, N))
+    rhs[:N, :] = np.eye(N)
+    sol = np.linalg.solve(M, rhs)
+    return K @ sol[:N] + T @ sol[N:]
+
+
+GCV_LOG10_GRID = -12.0 + 0.25 * np.arange(49)   # lambda = 10^-12 ... 10^0 (reading R16)
+
+
+def gcv_score(x, y, lam: float) -> float:
+    """Craven & Wahba GCV: V(lam) = (1/N)||(I - A)y||^2 / ((1/N) tr(I - A))^2."""
+    A = tps_influence(x, lam)
+    y = np.asarray(y, dtype=np.float64)
+    N = len(y)
+    res = y - A @ y
+    return (res @ res / N) / ((np.trace(np.eye(N) - A) / N) ** 2)
+
+
+def tps_smooth(x, y, lam: float = -1.0):
+    """Smoothed values P~ at the sites and the lambda used (lam < 0: GCV over the grid,
+    the first minimiser wins)."""
+    if lam < 0:
+        scores = np.array([gcv_score(x, y, 10.0 ** g) for g in GCV_LOG10_GRID])
+        lam = float(10.0 ** GCV_LOG10_GRID[int(np.argmin(scores))])
+    fitted, _, _ = tps_fit(x, y, lam)
+    return fitted, lam
+
+
+def argmax(values) -> int:
+    """Design with the largest value, lowest index on ties."""
+    v = np.asarray(values)
+    best = 0
+    for i in range(1, len(v)):
+        if v[i] > v[best]:
+            best = i
+    return best
