@@ -1,0 +1,237 @@
+// mc_device.cuh — device arithmetic of the fused Monte-Carlo kernel (sm_100a, fp32 + integer).
+//
+// Implements DESIGN.md §2.2-2.7 (the contract the independent oracle also implements):
+//   Philox4x32-10 word stream keyed (design, sample)          §2.2
+//   23-bit uniforms, Box-Muller on MUFU.{LG2,SQRT,SIN,COS}     §2.3
+//   prior draw Delta = theta + L_p eps  (Formula 10) §2.4, folded into b = zc - M eps
+//   utility u: COND (SOV normal CDFs) or IND (Formula 6/7)     §2.5, §2.6
+//   exact 2^-23 fixed-point accumulation                       §2.7
+#pragma once
+#include <cstdint>
+
+namespace mcd {
+
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
+// Geometry of one draw for N populations, prior dimension P = N, estimator EST (0 COND, 1 IND).
+template <int N, int EST>
+struct Geo {
+  static constexpr int P = N;
+  static constexpr int NNORM = (EST == 0) ? P : P + N;          // normals per draw
+  static constexpr int NPAIR = (NNORM + 1) / 2;                   // Box-Muller pairs
+  static constexpr int U = (EST == 0) ? 2 * ((P + 1) / 2) + (N - 1) : 2 * NPAIR;  // words per draw
+  static constexpr int L = 4 / cgcd(U, 4);                        // draws per Philox-aligned step
+  static constexpr int BLOCKS = U * L / 4;                        // Philox blocks per step
+  static constexpr int NM = N * (N + 1) / 2;                      // packed lower-triangular M
+  static constexpr int DUMP = NNORM + N + 1;                      // floats per dumped draw
+};
+
+// ---------------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11).  Counter (q_lo, q_hi, design, 0), key (seed_lo, seed_hi).
+struct Key { uint32_t k0, k1; };
+
+__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                             uint32_t k0, uint32_t k1) {
+  const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+  const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+  c0 = hi1 ^ c1 ^ k0;
+  c1 = lo1;
+  c2 = hi0 ^ c3 ^ k1;
+  c3 = lo0;
+}
+
+// One block for counter (q, design, 0).  The first round's c2-product depends only on the
+// design, so callers pass it precomputed (lo1d = M1*design, hi1d = umulhi(M1, design)).
+__device__ __forceinline__ void philox_block(uint64_t q, uint32_t lo1d, uint32_t hi1d, Key key,
+                                             uint32_t out[4]) {
+  const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32);
+  // round 1 with c2 = design, c3 = 0
+  uint32_t c0 = hi1d ^ q1 ^ key.k0;
+  uint32_t c1 = lo1d;
+  uint32_t c2 = __umulhi(0xD2511F53u, q0) ^ key.k1;
+  uint32_t c3 = 0xD2511F53u * q0;
+  uint32_t k0 = key.k0, k1 = key.k1;
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+    philox_round(c0, c1, c2, c3, k0, k1);
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+__device__ __forceinline__ uint32_t philox_word(uint64_t seed, uint32_t design, uint64_t w) {
+  Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t o[4];
+  philox_block(w >> 2, 0xCD9E8D57u * design, __umulhi(0xCD9E8D57u, design), key, o);
+  return o[w & 3];
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fast fp32 primitives on the SFU (MUFU) pipe.
+__device__ __forceinline__ float lg2_approx(float x) { float y; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float ex2_approx(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float rcp_approx(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float sqrt_approx(float x) { float y; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float sin_approx(float x) { float y; asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float cos_approx(float x) { float y; asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+// 1 + k 2^-23 in [1, 2) from the low 23 bits k of a Philox word (one LOP3): DESIGN.md §2.3.
+__device__ __forceinline__ float word_to_f12(uint32_t w) { return __uint_as_float((w & 0x007FFFFFu) | 0x3F800000u); }
+
+// Box-Muller pair from words (wr, wa): R = sqrt(-2 ln u_r), angle 2 pi u_a.
+// u_r = 2 - f(wr) in (0,1]; the angle is evaluated as 2 pi (u_a - 1/2) in [-pi, pi) (MUFU's
+// accurate range) and the pair negated: (R cos 2pi u_a, R sin 2pi u_a) = -(R cos x, R sin x).
+__device__ __forceinline__ void box_muller(uint32_t wr, uint32_t wa, float& n0, float& n1) {
+  const float ur = 2.0f - word_to_f12(wr);
+  const float t = fmaxf(-1.38629436112f * lg2_approx(ur), 0.0f);   // -2 ln u_r
+  const float mr = -sqrt_approx(t);
+  const float x = (word_to_f12(wa) - 1.5f) * 6.28318530718f;
+  n0 = mr * cos_approx(x);
+  n1 = mr * sin_approx(x);
+}
+
+// Upper normal tail q = Phi(-a) = erfc(a/sqrt2)/2 for a >= 0 (Press et al., Numerical Recipes,
+// erfcc: t = 1/(1 + z/2), erfc(z) = t exp(-z^2 + poly(t)), fractional error < 1.2e-7), with the
+// exponent's constants pre-multiplied by log2(e) and the 1/2 folded in (EX2 on MUFU).
+// Returns q and e = 1 - q (= Phi(a)) without cancellation for either sign of a.
+__device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
+  const float aa = fabsf(a);
+  const float t = rcp_approx(fmaf(aa, 0.353553390593f, 1.0f));
+  constexpr double L2E = 1.4426950408889634;   // log2(e)
+  float p = (float)(0.17087277 * L2E);
+  p = fmaf(p, t, (float)(-0.82215223 * L2E));
+  p = fmaf(p, t, (float)(1.48851587 * L2E));
+  p = fmaf(p, t, (float)(-1.13520398 * L2E));
+  p = fmaf(p, t, (float)(0.27886807 * L2E));
+  p = fmaf(p, t, (float)(-0.18628806 * L2E));
+  p = fmaf(p, t, (float)(0.09678418 * L2E));
+  p = fmaf(p, t, (float)(0.37409196 * L2E));
+  p = fmaf(p, t, (float)(1.00002368 * L2E));
+  p = fmaf(p, t, (float)(-1.26551223 * L2E - 1.0));   // the -1 is the 1/2 of Phi = erfc/2
+  const float ex = ex2_approx(fmaf(aa * aa, (float)(-0.5 * L2E), p));   // -z^2 log2e, z = a/sqrt2
+  const float qp = t * ex;                     // Phi(-|a|)
+  const float qc = 1.0f - qp;                  // Phi(|a|)
+  const bool pos = a >= 0.0f;
+  q = pos ? qp : qc;
+  e = pos ? qc : qp;
+}
+
+// Standard normal quantile Phi^{-1}(p) given p and its complement pc = 1 - p (both computed
+// accurately by the caller), via erfinv(y) = g(w) y, y = 2p - 1 = p - pc, w = -ln(4 p pc):
+// central (w < 5) and near-tail (w < 16) polynomials of M. Giles, "Approximating the erfinv
+// function" (GPU Computing Gems Jade, 2011); deep tail (w >= 16, p < 1.1e-7) our own fit
+// (tools/fit_erfinv_deep_tail.py).  Relative error < 6e-7 for p in (1e-38, 1).
+__device__ __forceinline__ float normal_quantile(float p, float pc) {
+  const float pp = fmaxf(p * pc, 1.0e-38f);
+  const float w = -0.69314718056f * (lg2_approx(pp) + 2.0f);
+  float g;
+  if (w < 5.0f) {
+    const float ww = w - 2.5f;
+    g = 2.81022636e-08f;
+    g = fmaf(g, ww, 3.43273939e-07f);
+    g = fmaf(g, ww, -3.5233877e-06f);
+    g = fmaf(g, ww, -4.39150654e-06f);
+    g = fmaf(g, ww, 0.00021858087f);
+    g = fmaf(g, ww, -0.00125372503f);
+    g = fmaf(g, ww, -0.00417768164f);
+    g = fmaf(g, ww, 0.246640727f);
+    g = fmaf(g, ww, 1.50140941f);
+  } else {
+    const float sw = sqrt_approx(fminf(w, 88.0f));
+    if (w < 16.0f) {
+      const float ww = sw - 3.0f;
+      g = -0.000200214257f;
+      g = fmaf(g, ww, 0.000100950558f);
+      g = fmaf(g, ww, 0.00134934322f);
+      g = fmaf(g, ww, -0.00367342844f);
+      g = fmaf(g, ww, 0.00573950773f);
+      g = fmaf(g, ww, -0.0076224613f);
+      g = fmaf(g, ww, 0.00943887047f);
+      g = fmaf(g, ww, 1.00167406f);
+      g = fmaf(g, ww, 2.83297682f);
+    } else {
+      const float ww = sw - 6.0f;
+      g = 7.926354328446905e-07f;
+      g = fmaf(g, ww, -6.932396900083404e-06f);
+      g = fmaf(g, ww, 2.5214179913746193e-05f);
+      g = fmaf(g, ww, -3.964155257563107e-05f);
+      g = fmaf(g, ww, -0.0004801170143764466f);
+      g = fmaf(g, ww, 1.0096029043197632f);
+      g = fmaf(g, ww, 5.859915256500244f);
+    }
+  }
+  return 1.41421356237f * g * (p - pc);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Per-problem parameters in registers (loaded once per tile; uniform across the block).
+template <int N>
+struct ProbRegs {
+  float M[N * (N + 1) / 2];   // M = diag(c) L_p, packed lower triangular (row i: M[i(i+1)/2 + j])
+  float rho[N > 1 ? N - 1 : 1], sd[N > 1 ? N - 1 : 1], isd[N > 1 ? N - 1 : 1];
+};
+
+// One draw from its U words w[0..U): returns u in [0,1].  If DBG, writes the normals, b and u.
+template <int N, int EST, bool DBG>
+__device__ __forceinline__ float draw_utility(const uint32_t* w, const float* zc, const ProbRegs<N>& pr,
+                                              float* dbg = nullptr) {
+  using G = Geo<N, EST>;
+  float nrm[2 * G::NPAIR];
+#pragma unroll
+  for (int j = 0; j < G::NPAIR; ++j) box_muller(w[2 * j], w[2 * j + 1], nrm[2 * j], nrm[2 * j + 1]);
+  // b_i = z_i - c_i Delta_i = (z_i - c_i theta_i) - sum_{j<=i} (c_i L_p,ij) eps_j   (Formulas 3-5, 10)
+  float b[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    float acc = zc[i];
+#pragma unroll
+    for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
+    b[i] = acc;
+  }
+  float u;
+  if constexpr (EST == 1) {
+    // Formula 6/7: one null draw X = L0 W (Markov recursion), success iff some X_i > b_i.
+    float x = nrm[G::P];
+    bool rej = x > b[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
+      x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * nrm[G::P + i]);
+      rej = rej || (x > b[i]);
+    }
+    u = rej ? 1.0f : 0.0f;
+  } else {
+    // COND: u = 1 - prod e_i accumulated as u <- u + (1 - u) q_i (q_i = 1 - e_i, no cancellation).
+    constexpr int VB = 2 * ((G::P + 1) / 2);
+    float q, e;
+    normal_tail(b[0], q, e);     // q = Phi(-b1) = P(X1 > b1), e = Phi(b1)
+    u = q;
+    float x = 0.0f;
+    if constexpr (N > 1) {
+      const float v = word_to_f12(w[VB]) - 0.99999994039535522f;      // (k + 1/2) 2^-23
+      const float vc = 1.0f - v;                                       // exact
+      x = normal_quantile(v * e, fmaf(v, q, vc));
+    }
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
+      const float m = pr.rho[i - 1] * x;
+      normal_tail((b[i] - m) * pr.isd[i - 1], q, e);
+      u = fmaf(1.0f - u, q, u);
+      if (i + 1 < N) {
+        const float v = word_to_f12(w[VB + i]) - 0.99999994039535522f;
+        const float vc = 1.0f - v;
+        x = fmaf(pr.sd[i - 1], normal_quantile(v * e, fmaf(v, q, vc)), m);
+      }
+    }
+  }
+  if constexpr (DBG) {
+#pragma unroll
+    for (int k = 0; k < G::NNORM; ++k) dbg[k] = nrm[k];
+#pragma unroll
+    for (int i = 0; i < N; ++i) dbg[G::NNORM + i] = b[i];
+    dbg[G::NNORM + N] = u;
+  }
+  return u;
+}
+
+}  // namespace mcd

@@ -1,0 +1,86 @@
+// mc_internal.h — library-internal context and launch helpers (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/mc_design.h"
+
+namespace mci {
+
+constexpr int PROB_STRIDE = 96;          // floats per device problem record
+constexpr int OFF_M = 0;                 // packed M = diag(c) L_p (55 floats for n = 10)
+constexpr int OFF_RHO = 56;              // rho_i = sqrt(r_{i+1}/r_i)
+constexpr int OFF_SD = 66;               // s_i = sqrt(1 - rho_i^2)
+constexpr int OFF_ISD = 76;              // 1/s_i
+constexpr int SAMPLES_PER_THREAD = 64;   // per-thread sample run inside a tile
+constexpr int MAX_BLOCK = 256;           // fused kernel __launch_bounds__
+
+void set_error(const std::string& msg);
+mc_status cuda_fail(cudaError_t e, const char* where);
+
+#define MC_CUDA(call)                                                   \
+  do {                                                                  \
+    cudaError_t _e = (call);                                            \
+    if (_e != cudaSuccess) return mci::cuda_fail(_e, #call);            \
+  } while (0)
+
+struct TpsPlan {
+  int64_t begin = 0;       // first design of the problem
+  int64_t count = 0;       // designs of the problem
+  int64_t nfit = 0;        // fitted designs (mask)
+  int32_t d = 0;           // TPS dimension
+  bool passthrough = true; // too few points / n == 1
+  double* fit_idx_dummy = nullptr;
+  int64_t* d_fit_idx = nullptr;   // [nfit] global design indices of the fitted designs
+  double* d_E = nullptr;          // [nfit x k] column-major, k = nfit - d - 1 (Q2 V)
+  double* d_lam = nullptr;        // [k] eigenvalues of Q2^T K Q2
+};
+
+}  // namespace mci
+
+struct mc_ctx {
+  int device = 0;
+  int n = 0;
+  int est = 0;
+  int32_t n_probs = 0;
+  int64_t D = 0;
+  uint64_t seed = 0;
+  std::vector<mc_problem> probs;
+  std::vector<double> alpha;             // host copy [D*n]
+  std::vector<int32_t> pod;              // host copy [D]
+  std::vector<int64_t> prob_begin;       // [n_probs+1]
+  float* d_prob = nullptr;               // [n_probs * PROB_STRIDE]
+  float* d_zc = nullptr;                 // [D * n]
+  int32_t* d_pod = nullptr;              // [D]
+  int64_t* d_prob_begin = nullptr;       // [n_probs+1]
+  int block_threads = 256;
+  int grid_blocks = 0;                   // 0 = auto
+  int64_t launches = 0;
+  bool plan_built = false;
+  std::vector<mci::TpsPlan> plans;
+  double* d_tps_scratch = nullptr;       // per-problem scratch for smoothing
+  size_t tps_scratch_elems = 0;
+};
+
+// launchers implemented in the .cu files
+namespace mci {
+mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
+                       int64_t* sums);
+mc_status launch_finalize(mc_ctx* c, const int64_t* sums, uint64_t N, double* mean, double* var, cudaStream_t st);
+mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64_t* word, int64_t count,
+                             uint32_t* out, cudaStream_t st);
+mc_status launch_draw_dump(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
+                           cudaStream_t st);
+int draw_dump_stride(int n, int est);
+int words_per_draw(int n, int est);
+mc_status launch_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, cudaStream_t st);
+mc_status alpha_grid_solve(const mc_problem* probs, int32_t n_probs, int32_t m, int device,
+                           std::vector<double>& alpha, std::vector<uint8_t>& valid);
+mc_status fwer_eval(const mc_problem* p, const double* alpha, int64_t count, double* out, int device);
+mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st);
+mc_status smooth_apply(mc_ctx* c, const double* values, double lambda, double* out, double* lam_used,
+                       cudaStream_t st);
+}  // namespace mci

@@ -1,0 +1,298 @@
+// mc_kernels.cu — K1 fused Monte-Carlo kernel, K2 finalize, K3 Philox dump, draw dump, K6 argmax.
+//
+// K1 (rows a2-a6 of DESIGN.md §1): persistent grid over tiles (design, 64*blockDim samples).
+// Each thread owns 64 consecutive samples of one design, generates their Philox words in
+// registers (U words per draw, L draws per aligned step), evaluates u, and accumulates the exact
+// 2^-23 fixed-point sums in 32-bit registers; a 64-bit warp shuffle + shared-memory block reduction
+// then issues one 64-bit atomicAdd pair per (block, design tile).  Integer sums make the result
+// independent of the launch shape.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "mc_device.cuh"
+#include "mc_internal.h"
+
+namespace mci {
+
+using namespace mcd;
+
+template <int N>
+__device__ __forceinline__ void load_problem(const float* __restrict__ rec, ProbRegs<N>& pr) {
+#pragma unroll
+  for (int k = 0; k < N * (N + 1) / 2; ++k) pr.M[k] = __ldg(rec + OFF_M + k);
+#pragma unroll
+  for (int k = 0; k < N - 1; ++k) {
+    pr.rho[k] = __ldg(rec + OFF_RHO + k);
+    pr.sd[k] = __ldg(rec + OFF_SD + k);
+    pr.isd[k] = __ldg(rec + OFF_ISD + k);
+  }
+}
+
+// fixed-point accumulation of one draw: q(x) = round-half-even(2^23 x) for x in [0,1] is the
+// mantissa of the fp32 sum x + 1 (one FADD / FFMA + one IADD3).
+__device__ __forceinline__ void accumulate(float u, uint32_t& a1, uint32_t& a2) {
+  a1 += __float_as_uint(u + 1.0f) - 0x3F800000u;
+  a2 += __float_as_uint(fmaf(u, u, 1.0f)) - 0x3F800000u;
+}
+
+template <int N, int EST, bool MASKED>
+__device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64_t E, uint32_t lo1d, uint32_t hi1d,
+                                            Key key, const float* zc, const ProbRegs<N>& pr, uint32_t& a1,
+                                            uint32_t& a2) {
+  using G = Geo<N, EST>;
+  constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
+  static_assert(SAMPLES_PER_THREAD % G::L == 0, "L must divide the per-thread run");
+  uint64_t q = s_begin * (uint64_t)G::U / 4;   // first Philox block of this thread's run
+#pragma unroll 1
+  for (int st = 0; st < STEPS; ++st) {
+    const uint64_t s0 = s_begin + (uint64_t)st * G::L;
+    if (MASKED && s0 >= E) break;
+    uint32_t w[G::BLOCKS * 4];
+#pragma unroll
+    for (int b = 0; b < G::BLOCKS; ++b) philox_block(q + b, lo1d, hi1d, key, &w[4 * b]);
+    q += G::BLOCKS;
+#pragma unroll
+    for (int l = 0; l < G::L; ++l) {
+      float u = draw_utility<N, EST, false>(&w[l * G::U], zc, pr);
+      if (MASKED) {
+        const uint64_t s = s0 + l;
+        u = (s >= B && s < E) ? u : 0.0f;
+      }
+      accumulate(u, a1, a2);
+    }
+  }
+}
+
+template <int N, int EST>
+__global__ void __launch_bounds__(MAX_BLOCK) mc_fused_kernel(const float* __restrict__ prob, const float* __restrict__ zc_all,
+                                                             const int32_t* __restrict__ pod, int64_t d0,
+                                                             uint64_t B, uint64_t E, uint64_t Balign,
+                                                             int64_t tiles_per_design, int64_t total_tiles,
+                                                             uint64_t seed, unsigned long long* __restrict__ sums) {
+  __shared__ unsigned long long red[2][MAX_BLOCK / 32];
+  const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint64_t tile_samples = (uint64_t)blockDim.x * SAMPLES_PER_THREAD;
+  for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    const int64_t d = d0 + tile / tiles_per_design;
+    const int64_t chunk = tile % tiles_per_design;
+    ProbRegs<N> pr;
+    load_problem<N>(prob + (int64_t)__ldg(pod + d) * PROB_STRIDE, pr);
+    float zc[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) zc[i] = __ldg(zc_all + d * N + i);
+    const uint32_t dd = (uint32_t)d;
+    const uint32_t lo1d = 0xCD9E8D57u * dd, hi1d = __umulhi(0xCD9E8D57u, dd);
+    const uint64_t s_begin = Balign + (uint64_t)chunk * tile_samples + (uint64_t)threadIdx.x * SAMPLES_PER_THREAD;
+    uint32_t a1 = 0, a2 = 0;
+    if (s_begin >= B && s_begin + SAMPLES_PER_THREAD <= E)
+      run_samples<N, EST, false>(s_begin, B, E, lo1d, hi1d, key, zc, pr, a1, a2);
+    else if (s_begin < E)
+      run_samples<N, EST, true>(s_begin, B, E, lo1d, hi1d, key, zc, pr, a1, a2);
+    unsigned long long v1 = a1, v2 = a2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+      v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    }
+    if (lane == 0) { red[0][warp] = v1; red[1][warp] = v2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t1 = 0, t2 = 0;
+      for (int k = 0; k < nwarps; ++k) { t1 += red[0][k]; t2 += red[1][k]; }
+      atomicAdd(sums + 2 * d, t1);
+      atomicAdd(sums + 2 * d + 1, t2);
+    }
+    __syncthreads();
+  }
+}
+
+template <int N, int EST>
+static cudaError_t launch_fused_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
+                                  int64_t* sums) {
+  using G = Geo<N, EST>;
+  const int threads = c->block_threads;
+  const uint64_t tile = (uint64_t)threads * SAMPLES_PER_THREAD;
+  const uint64_t Balign = B - (B % G::L);
+  const int64_t tpd = (int64_t)((E - Balign + tile - 1) / tile);
+  const int64_t total = tpd * dcount;
+  int grid = c->grid_blocks;
+  if (grid <= 0) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mc_fused_kernel<N, EST>, threads, 0);
+    grid = nsm * (per > 0 ? per : 1);
+  }
+  if ((int64_t)grid > total) grid = (int)total;
+  if (grid <= 0) return cudaSuccess;
+  mc_fused_kernel<N, EST><<<grid, threads, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, d0, B, E, Balign, tpd, total,
+                                                    c->seed, reinterpret_cast<unsigned long long*>(sums));
+  c->launches += 1;
+  return cudaGetLastError();
+}
+
+#define MC_DISPATCH_N(FN, ...)                                                  \
+  switch (c->n) {                                                               \
+    case 1: e = FN<1, EST>(__VA_ARGS__); break;                                 \
+    case 2: e = FN<2, EST>(__VA_ARGS__); break;                                 \
+    case 3: e = FN<3, EST>(__VA_ARGS__); break;                                 \
+    case 4: e = FN<4, EST>(__VA_ARGS__); break;                                 \
+    case 5: e = FN<5, EST>(__VA_ARGS__); break;                                 \
+    case 6: e = FN<6, EST>(__VA_ARGS__); break;                                 \
+    case 7: e = FN<7, EST>(__VA_ARGS__); break;                                 \
+    case 8: e = FN<8, EST>(__VA_ARGS__); break;                                 \
+    case 9: e = FN<9, EST>(__VA_ARGS__); break;                                 \
+    case 10: e = FN<10, EST>(__VA_ARGS__); break;                               \
+    default: set_error("n out of range"); return MC_ERR_INVALID;                \
+  }
+
+template <int EST>
+static mc_status launch_fused_est(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
+                                  int64_t* sums) {
+  cudaError_t e = cudaSuccess;
+  MC_DISPATCH_N(launch_fused_t, c, d0, dcount, B, E, st, sums);
+  if (e != cudaSuccess) return cuda_fail(e, "mc_fused_kernel launch");
+  return MC_OK;
+}
+
+mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st, int64_t* sums) {
+  if (dcount <= 0 || E <= B) return MC_OK;
+  return c->est == 0 ? launch_fused_est<0>(c, d0, dcount, B, E, st, sums)
+                     : launch_fused_est<1>(c, d0, dcount, B, E, st, sums);
+}
+
+int words_per_draw(int n, int est) {
+  // Geo<N,EST>::U without instantiating every N
+  return est == 0 ? 2 * ((n + 1) / 2) + (n - 1) : 2 * ((2 * n + 1) / 2);
+}
+int draw_dump_stride(int n, int est) { return (est == 0 ? n : 2 * n) + n + 1; }
+
+// ---------------------------------------------------------------------------------------------
+// K2: finalize (row a8), fp64.
+__global__ void k_finalize(const long long* __restrict__ sums, int64_t D, double N, double* __restrict__ mean,
+                           double* __restrict__ var) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  const double scale = 1.0 / (N * 8388608.0);
+  const double m = (double)sums[2 * d] * scale;
+  const double m2 = (double)sums[2 * d + 1] * scale;
+  mean[d] = m;
+  if (var) var[d] = N > 1.0 ? (m2 - m * m) * N / (N - 1.0) : 0.0;
+}
+
+mc_status launch_finalize(mc_ctx* c, const int64_t* sums, uint64_t N, double* mean, double* var, cudaStream_t st) {
+  if (c->D == 0) return MC_OK;
+  const int threads = 256;
+  const int64_t blocks = (c->D + threads - 1) / threads;
+  k_finalize<<<(unsigned)blocks, threads, 0, st>>>(reinterpret_cast<const long long*>(sums), c->D, (double)N, mean, var);
+  MC_CUDA(cudaGetLastError());
+  return MC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K3: Philox words (test hook).
+__global__ void k_philox_dump(uint64_t seed, const uint32_t* __restrict__ design, const uint64_t* __restrict__ word,
+                              int64_t count, uint32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < count) out[i] = philox_word(seed, design[i], word[i]);
+}
+
+mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64_t* word, int64_t count, uint32_t* out,
+                             cudaStream_t st) {
+  if (count <= 0) return MC_OK;
+  k_philox_dump<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(seed, design, word, count, out);
+  MC_CUDA(cudaGetLastError());
+  return MC_OK;
+}
+
+// Per-draw dump through the fused kernel's draw_utility (test hook).
+template <int N, int EST>
+__global__ void k_draw_dump(const float* __restrict__ prob, const float* __restrict__ zc_all,
+                            const int32_t* __restrict__ pod, uint64_t seed, const int64_t* __restrict__ design,
+                            const uint64_t* __restrict__ sample, int64_t count, float* __restrict__ out) {
+  using G = Geo<N, EST>;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int64_t d = design[i];
+  ProbRegs<N> pr;
+  load_problem<N>(prob + (int64_t)pod[d] * PROB_STRIDE, pr);
+  float zc[N];
+  for (int k = 0; k < N; ++k) zc[k] = zc_all[d * N + k];
+  uint32_t w[G::U];
+  const uint64_t base = sample[i] * (uint64_t)G::U;
+  for (int k = 0; k < G::U; ++k) w[k] = philox_word(seed, (uint32_t)d, base + k);
+  draw_utility<N, EST, true>(w, zc, pr, out + i * G::DUMP);
+}
+
+template <int N, int EST>
+static cudaError_t launch_dump_t(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
+                                 cudaStream_t st) {
+  k_draw_dump<N, EST><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, c->seed, design,
+                                                                      sample, count, out);
+  return cudaGetLastError();
+}
+
+template <int EST>
+static mc_status launch_dump_est(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
+                                 cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  MC_DISPATCH_N(launch_dump_t, c, design, sample, count, out, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_draw_dump launch");
+  return MC_OK;
+}
+
+mc_status launch_draw_dump(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
+                           cudaStream_t st) {
+  if (count <= 0) return MC_OK;
+  return c->est == 0 ? launch_dump_est<0>(c, design, sample, count, out, st)
+                     : launch_dump_est<1>(c, design, sample, count, out, st);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K6: segmented argmax (row a10): one block per problem, lexicographic (max value, min index).
+__device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t bi) {
+  if (v != v) return false;                 // NaN never wins
+  if (bv != bv) return true;
+  return v > bv || (v == bv && i < bi);
+}
+
+__global__ void k_segmented_argmax(const double* __restrict__ values, const int64_t* __restrict__ begin,
+                                   int64_t* __restrict__ idx, double* __restrict__ val) {
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  const int p = blockIdx.x;
+  const int64_t b = begin[p], e = begin[p + 1];
+  double bv = __longlong_as_double(0xFFF8000000000000ull);   // NaN = empty
+  int64_t bi = -1;
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    const double v = values[i];
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, (long long)bi, o);
+    if (oi >= 0 && (bi < 0 || better(ov, oi, bv, bi))) { bv = ov; bi = oi; }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (si[k] >= 0 && (bi < 0 || better(sv[k], si[k], bv, bi))) { bv = sv[k]; bi = si[k]; }
+    idx[p] = bi;
+    val[p] = bv;
+  }
+}
+
+mc_status launch_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, cudaStream_t st) {
+  if (c->n_probs == 0) return MC_OK;
+  k_segmented_argmax<<<c->n_probs, 256, 0, st>>>(values, c->d_prob_begin, idx, val);
+  MC_CUDA(cudaGetLastError());
+  return MC_OK;
+}
+
+}  // namespace mci

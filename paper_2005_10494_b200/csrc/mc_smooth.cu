@@ -1,0 +1,424 @@
+// mc_smooth.cu — K5: thin-plate-spline smoothing of the noisy power surface with GCV
+// (Sec. 2.3; row a9 of DESIGN.md §1; contract DESIGN.md §2.9).
+//
+// Plan (once per design set, per problem with N fitted sites x = alpha_{1..d}/alpha0, d = n-1):
+//   K_ij = phi(|x_i - x_j|) (fp64 kernel), T = [1 x] = Q R (host Householder, k = d+1 reflectors),
+//   B = (Q^T K Q)[k:, k:] = V Lambda V^T (cuSOLVER Dsyevd), E = Q[:, k:] V  (N x (N-k), kept in HBM).
+// Apply (every evaluation): c = E^T y; GCV(lambda) = N sum_j (t_j c_j)^2 / (sum_j t_j)^2 with
+//   t_j = N lambda / (Lambda_j + N lambda) over the fixed log grid; y~ = y - E (t .* c).
+// This is the penalised TPS [K + N lambda I, T; T^T, 0][w; beta] = [y; 0] (y~ = y - N lambda w)
+// written in the eigenbasis, so one plan serves every lambda and every evaluation.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "mc_internal.h"
+
+namespace mci {
+
+constexpr int GCV_K = 49;   // lambda = 10^(-12 + 0.25 k), k = 0..48 (reading R16)
+
+__device__ __forceinline__ double tps_phi(double r, int d) {
+  if (d == 1) return r * r * r;
+  if (d == 2) return r > 0.0 ? r * r * log(r) : 0.0;
+  return -r;   // d = 3
+}
+
+__global__ void k_tps_kernel_matrix(const double* __restrict__ X, int64_t N, int d, double* __restrict__ K) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // row
+  const int64_t j = blockIdx.y;                                        // column
+  if (i >= N) return;
+  double r2 = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = X[i * d + k] - X[j * d + k];
+    r2 += t * t;
+  }
+  K[i + j * N] = tps_phi(sqrt(r2), d);
+}
+
+// w_j = sum_i v_i A_ij (column dots), one block per column
+__global__ void k_col_dot(const double* __restrict__ A, int64_t N, int64_t ncols, int64_t lda,
+                          const double* __restrict__ v, double* __restrict__ w) {
+  __shared__ double sh[32];
+  const int64_t j = blockIdx.x;
+  if (j >= ncols) return;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) acc += v[i] * A[i + j * lda];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+    w[j] = t;
+  }
+}
+
+// A <- A - tau v w^T  (left Householder application: (I - tau v v^T) A with w = A^T v)
+__global__ void k_rank1_left(double* __restrict__ A, int64_t N, int64_t ncols, int64_t lda, const double* __restrict__ v,
+                             const double* __restrict__ w, double tau) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (i < N && j < ncols) A[i + j * lda] -= tau * v[i] * w[j];
+}
+
+// Two-sided symmetric update A <- H A H, H = I - tau v v^T (LAPACK sytrd form):
+// p = tau A v (from k_col_dot, A symmetric), w = p - (tau/2)(p^T v) v, A <- A - v w^T - w v^T.
+__global__ void k_sym_w(const double* __restrict__ Av, const double* __restrict__ v, int64_t N, double tau,
+                        double* __restrict__ w) {
+  __shared__ double sh[32];
+  __shared__ double s_alpha;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) acc += tau * Av[i] * v[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+    s_alpha = 0.5 * tau * t;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) w[i] = tau * Av[i] - s_alpha * v[i];
+}
+
+__global__ void k_rank2(double* __restrict__ A, int64_t N, const double* __restrict__ v, const double* __restrict__ w) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (i < N) A[i + j * N] -= v[i] * w[j] + w[i] * v[j];
+}
+
+__global__ void k_embed(const double* __restrict__ V, int64_t N, int k, double* __restrict__ Z) {
+  // Z (N x (N-k)) = [0_{k x (N-k)}; V], V = (N-k) x (N-k) with lda = N at offset (k, k) of the K buffer
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (i >= N) return;
+  Z[i + j * N] = i < k ? 0.0 : V[(i - k) + j * N];
+}
+
+// ---- apply-side kernels, batched over problems (blockIdx.y or blockIdx.x = problem) ----------
+struct PlanDev {
+  const double* E;
+  const double* lam;
+  const int64_t* fit_idx;
+  int64_t N;      // fitted sites
+  int64_t k;      // N - (d+1) eigen-columns
+  int64_t off;    // offset into the c / y scratch
+};
+
+__global__ void k_gather(const PlanDev* __restrict__ pl, const double* __restrict__ values, double* __restrict__ y) {
+  const PlanDev p = pl[blockIdx.y];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.N; i += (int64_t)gridDim.x * blockDim.x)
+    y[p.off + i] = values[p.fit_idx[i]];
+}
+
+// c_j = sum_i E_ij y_i  (column j contiguous), one warp per column
+__global__ void k_et_y(const PlanDev* __restrict__ pl, const double* __restrict__ y, double* __restrict__ c) {
+  const PlanDev p = pl[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= p.k) return;
+  const double* col = p.E + j * p.N;
+  const double* yy = y + p.off;
+  double acc = 0.0;
+  for (int64_t i = lane; i < p.N; i += 32) acc += col[i] * yy[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) c[p.off + j] = acc;
+}
+
+// GCV over the log grid (or the fixed lambda), then c_j <- t_j c_j.  One block per problem.
+__global__ void k_gcv(const PlanDev* __restrict__ pl, double lambda_fixed, double* __restrict__ c,
+                      double* __restrict__ lam_used) {
+  __shared__ double s_rss[32], s_tr[32];
+  __shared__ double s_best;
+  const PlanDev p = pl[blockIdx.x];
+  const double Nd = (double)p.N;
+  double lam = lambda_fixed;
+  if (lambda_fixed < 0.0) {
+    double best = INFINITY, bestlam = 0.0;
+    for (int g = 0; g < GCV_K; ++g) {
+      const double l = pow(10.0, -12.0 + 0.25 * g);
+      const double nl = Nd * l;
+      double rss = 0.0, tr = 0.0;
+      for (int64_t j = threadIdx.x; j < p.k; j += blockDim.x) {
+        const double t = nl / (p.lam[j] + nl);
+        const double tc = t * c[p.off + j];
+        rss += tc * tc;
+        tr += t;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        rss += __shfl_xor_sync(0xffffffffu, rss, o);
+        tr += __shfl_xor_sync(0xffffffffu, tr, o);
+      }
+      if ((threadIdx.x & 31) == 0) { s_rss[threadIdx.x >> 5] = rss; s_tr[threadIdx.x >> 5] = tr; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double R = 0.0, T = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { R += s_rss[k]; T += s_tr[k]; }
+        const double v = Nd * R / (T * T);
+        if (v < best) { best = v; bestlam = l; }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) s_best = bestlam;
+    __syncthreads();
+    lam = s_best;
+  }
+  if (threadIdx.x == 0 && lam_used) lam_used[blockIdx.x] = lam;
+  const double nl = Nd * lam;
+  for (int64_t j = threadIdx.x; j < p.k; j += blockDim.x) c[p.off + j] *= nl / (p.lam[j] + nl);
+}
+
+// out[fit_idx[i]] = y_i - sum_j E_ij c_j   (thread per row; the j-loop reads E coalesced)
+__global__ void k_e_c(const PlanDev* __restrict__ pl, const double* __restrict__ y, const double* __restrict__ c,
+                      double* __restrict__ out) {
+  const PlanDev p = pl[blockIdx.y];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  const double* cc = c + p.off;
+  double acc = 0.0;
+  for (int64_t j = 0; j < p.k; ++j) acc += p.E[i + j * p.N] * cc[j];
+  out[p.fit_idx[i]] = y[p.off + i] - acc;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Householder QR of T = [1 x] (N x k, fp64, host): returns reflectors v_r (v_r[r] = 1) and tau_r.
+static void householder_T(const std::vector<double>& X, int64_t N, int d, std::vector<double>& V,
+                          std::vector<double>& tau) {
+  const int k = d + 1;
+  std::vector<double> T((size_t)N * k);
+  for (int64_t i = 0; i < N; ++i) {
+    T[i] = 1.0;
+    for (int c = 0; c < d; ++c) T[i + (c + 1) * N] = X[i * d + c];
+  }
+  V.assign((size_t)N * k, 0.0);
+  tau.assign(k, 0.0);
+  for (int r = 0; r < k; ++r) {
+    double nrm = 0.0;
+    for (int64_t i = r; i < N; ++i) nrm += T[i + r * N] * T[i + r * N];
+    nrm = std::sqrt(nrm);
+    const double a = T[r + r * N];
+    const double alpha = a >= 0 ? -nrm : nrm;
+    const double v0 = a - alpha;
+    // v = (T[r:, r] - alpha e_r) / v0 so that v[r] = 1
+    for (int64_t i = 0; i < N; ++i) V[i + r * N] = i < r ? 0.0 : (i == r ? 1.0 : T[i + r * N] / v0);
+    double vv = 0.0;
+    for (int64_t i = r; i < N; ++i) vv += V[i + r * N] * V[i + r * N];
+    tau[r] = 2.0 / vv;
+    for (int c = r; c < k; ++c) {
+      double s = 0.0;
+      for (int64_t i = r; i < N; ++i) s += V[i + r * N] * T[i + c * N];
+      for (int64_t i = r; i < N; ++i) T[i + c * N] -= tau[r] * V[i + r * N] * s;
+    }
+  }
+}
+
+#define MC_SOLVER(call)                                                              \
+  do {                                                                               \
+    cusolverStatus_t _s = (call);                                                    \
+    if (_s != CUSOLVER_STATUS_SUCCESS) {                                             \
+      set_error(std::string("cuSOLVER error ") + std::to_string((int)_s) + " in " #call); \
+      return MC_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+static mc_status build_one(mc_ctx* c, cusolverDnHandle_t h, cudaStream_t st, TpsPlan& pl, const std::vector<int64_t>& fit,
+                           double* d_K, double* d_work, int lwork, int* d_info, double* d_vec) {
+  const int n = c->n, d = n - 1, k = d + 1;
+  const int64_t N = (int64_t)fit.size();
+  const double a0 = c->probs[c->pod[fit[0]]].alpha0;
+  std::vector<double> X((size_t)N * d);
+  for (int64_t i = 0; i < N; ++i)
+    for (int j = 0; j < d; ++j) X[i * d + j] = c->alpha[fit[i] * n + j] / a0;
+  std::vector<double> Vh, tau;
+  householder_T(X, N, d, Vh, tau);
+  double *d_X = nullptr, *d_V = nullptr, *d_w = nullptr, *d_p = nullptr;
+  MC_CUDA(cudaMalloc(&d_X, sizeof(double) * N * d));
+  MC_CUDA(cudaMalloc(&d_V, sizeof(double) * N * k));
+  MC_CUDA(cudaMalloc(&d_w, sizeof(double) * N));
+  MC_CUDA(cudaMalloc(&d_p, sizeof(double) * N));
+  MC_CUDA(cudaMemcpyAsync(d_X, X.data(), sizeof(double) * N * d, cudaMemcpyHostToDevice, st));
+  MC_CUDA(cudaMemcpyAsync(d_V, Vh.data(), sizeof(double) * N * k, cudaMemcpyHostToDevice, st));
+  const dim3 g2((unsigned)((N + 255) / 256), (unsigned)N);
+  k_tps_kernel_matrix<<<g2, 256, 0, st>>>(d_X, N, d, d_K);
+  // B_full = H_k..H_1 K H_1..H_k
+  for (int r = 0; r < k; ++r) {
+    const double* v = d_V + (int64_t)r * N;
+    k_col_dot<<<(unsigned)N, 256, 0, st>>>(d_K, N, N, N, v, d_p);   // A v (A symmetric)
+    k_sym_w<<<1, 1024, 0, st>>>(d_p, v, N, tau[r], d_w);
+    k_rank2<<<g2, 256, 0, st>>>(d_K, N, v, d_w);
+  }
+  MC_CUDA(cudaGetLastError());
+  const int64_t m = N - k;
+  double* B = d_K + k + (int64_t)k * N;
+  MC_CUDA(cudaMalloc(&pl.d_lam, sizeof(double) * m));
+  MC_SOLVER(cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)m, B, (int)N, pl.d_lam, d_work,
+                             lwork, d_info));
+  int info = 0;
+  MC_CUDA(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MC_CUDA(cudaStreamSynchronize(st));
+  if (info != 0) {
+    set_error("mc_smooth_plan: Dsyevd failed (info = " + std::to_string(info) + ")");
+    return MC_ERR_NUMERIC;
+  }
+  // E = H_1 .. H_k [0; V]
+  MC_CUDA(cudaMalloc(&pl.d_E, sizeof(double) * N * m));
+  const dim3 g3((unsigned)((N + 255) / 256), (unsigned)m);
+  k_embed<<<g3, 256, 0, st>>>(B, N, k, pl.d_E);
+  for (int r = k - 1; r >= 0; --r) {
+    const double* v = d_V + (int64_t)r * N;
+    k_col_dot<<<(unsigned)m, 256, 0, st>>>(pl.d_E, N, m, N, v, d_vec);
+    k_rank1_left<<<g3, 256, 0, st>>>(pl.d_E, N, m, N, v, d_vec, tau[r]);
+  }
+  MC_CUDA(cudaGetLastError());
+  MC_CUDA(cudaMalloc(&pl.d_fit_idx, sizeof(int64_t) * N));
+  MC_CUDA(cudaMemcpyAsync(pl.d_fit_idx, fit.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, st));
+  MC_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_X);
+  cudaFree(d_V);
+  cudaFree(d_w);
+  cudaFree(d_p);
+  pl.nfit = N;
+  pl.d = d;
+  pl.passthrough = false;
+  return MC_OK;
+}
+
+mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
+  for (auto& pl : c->plans) {
+    cudaFree(pl.d_fit_idx);
+    cudaFree(pl.d_E);
+    cudaFree(pl.d_lam);
+  }
+  c->plans.assign(c->n_probs, TpsPlan{});
+  c->plan_built = false;
+  const int d = c->n - 1;
+  if (d > 3) {
+    set_error("mc_smooth_plan: TPS over more than 3 free alpha coordinates is not supported (n <= 4)");
+    return MC_ERR_INVALID;
+  }
+  // fitted sets and the largest one (for scratch sizing)
+  std::vector<std::vector<int64_t>> fits(c->n_probs);
+  int64_t Nmax = 0;
+  for (int k = 0; k < c->n_probs; ++k) {
+    TpsPlan& pl = c->plans[k];
+    pl.begin = c->prob_begin[k];
+    pl.count = c->prob_begin[k + 1] - c->prob_begin[k];
+    for (int64_t i = pl.begin; i < pl.begin + pl.count; ++i)
+      if (!mask || mask[i]) fits[k].push_back(i);
+    if (d >= 1 && (int64_t)fits[k].size() >= d + 2) Nmax = std::max<int64_t>(Nmax, (int64_t)fits[k].size());
+  }
+  if (Nmax > 0) {
+    cusolverDnHandle_t h;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) { set_error("cusolverDnCreate failed"); return MC_ERR_CUDA; }
+    cusolverDnSetStream(h, st);
+    double *d_K = nullptr, *d_work = nullptr, *d_vec = nullptr, *d_lam_tmp = nullptr;
+    int* d_info = nullptr;
+    int lwork = 0;
+    mc_status s = MC_OK;
+    cudaError_t e;
+    if ((e = cudaMalloc(&d_K, sizeof(double) * Nmax * Nmax)) != cudaSuccess ||
+        (e = cudaMalloc(&d_vec, sizeof(double) * Nmax)) != cudaSuccess ||
+        (e = cudaMalloc(&d_lam_tmp, sizeof(double) * Nmax)) != cudaSuccess ||
+        (e = cudaMalloc(&d_info, sizeof(int))) != cudaSuccess) {
+      s = cuda_fail(e, "mc_smooth_plan alloc");
+    } else {
+      const int m = (int)(Nmax - (d + 1));
+      if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, d_K, (int)Nmax, d_lam_tmp,
+                                      &lwork) != CUSOLVER_STATUS_SUCCESS) {
+        set_error("cusolverDnDsyevd_bufferSize failed");
+        s = MC_ERR_CUDA;
+      } else if ((e = cudaMalloc(&d_work, sizeof(double) * (size_t)lwork)) != cudaSuccess) {
+        s = cuda_fail(e, "mc_smooth_plan workspace");
+      }
+    }
+    for (int k = 0; s == MC_OK && k < c->n_probs; ++k) {
+      if ((int64_t)fits[k].size() < d + 2) continue;
+      // workspace for this size may be smaller than for Nmax: query and grow if needed
+      int lw = 0;
+      const int64_t N = (int64_t)fits[k].size();
+      cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)(N - d - 1), d_K, (int)N,
+                                  d_lam_tmp, &lw);
+      if (lw > lwork) {
+        cudaFree(d_work);
+        lwork = lw;
+        if ((e = cudaMalloc(&d_work, sizeof(double) * (size_t)lwork)) != cudaSuccess) { s = cuda_fail(e, "workspace"); break; }
+      }
+      s = build_one(c, h, st, c->plans[k], fits[k], d_K, d_work, lwork, d_info, d_vec);
+    }
+    cudaFree(d_K);
+    cudaFree(d_work);
+    cudaFree(d_vec);
+    cudaFree(d_lam_tmp);
+    cudaFree(d_info);
+    cusolverDnDestroy(h);
+    if (s != MC_OK) return s;
+  }
+  // scratch for y and c: sum of fitted sizes
+  int64_t tot = 0;
+  for (auto& pl : c->plans) tot += pl.passthrough ? 0 : pl.nfit;
+  cudaFree(c->d_tps_scratch);
+  c->d_tps_scratch = nullptr;
+  c->tps_scratch_elems = 0;
+  if (tot > 0) {
+    // y [tot], c [tot], PlanDev table
+    const size_t bytes = sizeof(double) * 2 * tot + sizeof(PlanDev) * c->n_probs + 64;
+    MC_CUDA(cudaMalloc(&c->d_tps_scratch, bytes));
+    c->tps_scratch_elems = (size_t)tot;
+    std::vector<PlanDev> pd;
+    int64_t off = 0;
+    for (auto& pl : c->plans) {
+      if (pl.passthrough) continue;
+      pd.push_back(PlanDev{pl.d_E, pl.d_lam, pl.d_fit_idx, pl.nfit, pl.nfit - pl.d - 1, off});
+      off += pl.nfit;
+    }
+    MC_CUDA(cudaMemcpy(reinterpret_cast<char*>(c->d_tps_scratch) + sizeof(double) * 2 * tot, pd.data(),
+                       sizeof(PlanDev) * pd.size(), cudaMemcpyHostToDevice));
+  }
+  c->plan_built = true;
+  return MC_OK;
+}
+
+mc_status smooth_apply(mc_ctx* c, const double* values, double lambda, double* out, double* lam_used, cudaStream_t st) {
+  // pass-through for every design first (designs outside any fit keep P~ = P^)
+  MC_CUDA(cudaMemcpyAsync(out, values, sizeof(double) * c->D, cudaMemcpyDeviceToDevice, st));
+  int np = 0;
+  int64_t Nmax = 0, kmax = 0;
+  for (auto& pl : c->plans)
+    if (!pl.passthrough) {
+      ++np;
+      Nmax = std::max(Nmax, pl.nfit);
+      kmax = std::max(kmax, pl.nfit - pl.d - 1);
+    }
+  if (lam_used) {
+    // problems without a fit report lambda = 0 (interpolation / pass-through)
+    MC_CUDA(cudaMemsetAsync(lam_used, 0, sizeof(double) * c->n_probs, st));
+  }
+  if (np == 0 || lambda == 0.0) return MC_OK;
+  const int64_t tot = (int64_t)c->tps_scratch_elems;
+  double* y = c->d_tps_scratch;
+  double* cc = y + tot;
+  const PlanDev* pd = reinterpret_cast<const PlanDev*>(reinterpret_cast<char*>(c->d_tps_scratch) + sizeof(double) * 2 * tot);
+  double* lam_tmp = nullptr;
+  if (lam_used) MC_CUDA(cudaMallocAsync(&lam_tmp, sizeof(double) * np, st));
+  k_gather<<<dim3(8, np), 256, 0, st>>>(pd, values, y);
+  k_et_y<<<dim3((unsigned)((kmax + 7) / 8), np), 256, 0, st>>>(pd, y, cc);
+  k_gcv<<<np, 256, 0, st>>>(pd, lambda, cc, lam_tmp);
+  k_e_c<<<dim3((unsigned)((Nmax + 127) / 128), np), 128, 0, st>>>(pd, y, cc, out);
+  MC_CUDA(cudaGetLastError());
+  if (lam_used) {
+    // scatter per-plan lambdas to their problem slots
+    std::vector<int> slot;
+    for (int k = 0; k < c->n_probs; ++k)
+      if (!c->plans[k].passthrough) slot.push_back(k);
+    for (int i = 0; i < np; ++i)
+      MC_CUDA(cudaMemcpyAsync(lam_used + slot[i], lam_tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    MC_CUDA(cudaFreeAsync(lam_tmp, st));
+  }
+  return MC_OK;
+}
+
+}  // namespace mci

@@ -1,0 +1,350 @@
+"""Thin ctypes binding of libmc_design.so (include/mc_design.h).
+
+Argument marshalling only: every step of the method runs in the CUDA library.  Torch supplies
+device memory (tensor ``data_ptr()``), the current CUDA stream and ``torch.distributed`` for the
+one cross-GPU combine (row a7).  There is no CPU fallback: compute calls raise if the library or a
+CUDA device is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+MC_MAX_N = 10
+EST_COND, EST_IND = 0, 1
+_STATUS = {0: "MC_OK", 1: "MC_ERR_INVALID", 2: "MC_ERR_NUMERIC", 3: "MC_ERR_INFEASIBLE", 4: "MC_ERR_CUDA",
+           5: "MC_ERR_OOM"}
+
+
+class McError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class mc_problem(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("has_prior_chol", ctypes.c_int32), ("i3", ctypes.c_double),
+                ("alpha0", ctypes.c_double), ("r", ctypes.c_double * MC_MAX_N),
+                ("theta", ctypes.c_double * MC_MAX_N), ("sigma", ctypes.c_double * MC_MAX_N),
+                ("prior_chol", ctypes.c_double * (MC_MAX_N * MC_MAX_N))]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_build.LIB):
+            raise RuntimeError(f"{_build.LIB} is missing: run `python -m paper_2005_10494_b200.build` "
+                               "(no CPU fallback exists)")
+        L = ctypes.CDLL(_build.LIB)
+        i32, i64, u64, d, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+        P = ctypes.POINTER
+        L.mc_last_error.restype = ctypes.c_char_p
+        L.mc_version.restype = ctypes.c_char_p
+        L.mc_information_units.argtypes = [d, d, d]; L.mc_information_units.restype = d
+        L.mc_threshold.argtypes = [d]; L.mc_threshold.restype = d
+        L.mc_problem_formula10.argtypes = [i32, P(d), P(d), d, d, P(mc_problem)]; L.mc_problem_formula10.restype = i32
+        L.mc_fwer.argtypes = [P(mc_problem), P(d), i64, P(d), i32]; L.mc_fwer.restype = i32
+        L.mc_candidates.argtypes = [P(mc_problem), i32, i32, i64, u64, P(d), P(i32), i64, P(i64), i32]
+        L.mc_candidates.restype = i32
+        L.mc_design_init.argtypes = [P(vp), P(mc_problem), i32, P(d), P(i32), i64, u64, i32, i32]
+        L.mc_design_init.restype = i32
+        L.mc_set_launch.argtypes = [vp, i32, i32]; L.mc_set_launch.restype = i32
+        L.mc_destroy.argtypes = [vp]; L.mc_destroy.restype = None
+        L.mc_evaluate_grid.argtypes = [vp, i64, i64, u64, u64, vp, vp]; L.mc_evaluate_grid.restype = i32
+        L.mc_finalize.argtypes = [vp, vp, u64, vp, vp, vp]; L.mc_finalize.restype = i32
+        L.mc_smooth_plan.argtypes = [vp, vp, vp]; L.mc_smooth_plan.restype = i32
+        L.mc_smooth.argtypes = [vp, vp, d, vp, vp, vp]; L.mc_smooth.restype = i32
+        L.mc_argmax.argtypes = [vp, vp, vp, vp, P(i64), P(d), vp]; L.mc_argmax.restype = i32
+        L.mc_num_designs.argtypes = [vp]; L.mc_num_designs.restype = i64
+        L.mc_num_problems.argtypes = [vp]; L.mc_num_problems.restype = i32
+        L.mc_words_per_draw.argtypes = [vp]; L.mc_words_per_draw.restype = i32
+        L.mc_philox_dump.argtypes = [u64, vp, vp, i64, vp, vp]; L.mc_philox_dump.restype = i32
+        L.mc_draw_dump.argtypes = [vp, vp, vp, i64, vp, vp]; L.mc_draw_dump.restype = i32
+        L.mc_draw_dump_stride.argtypes = [vp]; L.mc_draw_dump_stride.restype = i32
+        L.mc_kernel_launches.argtypes = [vp]; L.mc_kernel_launches.restype = i64
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_fwer", "mc_candidates",
+            "mc_design_init", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
+            "mc_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
+            "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
+
+
+def _check(status: int):
+    if status != 0:
+        raise McError(status, lib().mc_last_error().decode())
+
+
+def _dp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2005_10494_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    return torch
+
+
+def _stream(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# ------------------------------------------------------------------------------------------
+# problem helpers (host fp64, inside the library)
+
+def information_units(alpha: float = 0.025, beta: float = 0.1, delta: float = 0.2) -> float:
+    return float(lib().mc_information_units(alpha, beta, delta))
+
+
+def threshold(alpha: float) -> float:
+    return float(lib().mc_threshold(alpha))
+
+
+def problem_formula10(r, delta0, i3: float, alpha0: float = 0.025) -> mc_problem:
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    d0 = np.ascontiguousarray(delta0, dtype=np.float64)
+    p = mc_problem()
+    _check(lib().mc_problem_formula10(len(r), _dp(r), _dp(d0), float(i3), float(alpha0), ctypes.byref(p)))
+    return p
+
+
+def problem_general(r, theta, prior_chol, i3: float, alpha0: float = 0.025) -> mc_problem:
+    """A Gaussian prior N(theta, L L^T) given by its lower Cholesky factor L (n x n)."""
+    p = mc_problem()
+    n = len(r)
+    p.n, p.has_prior_chol, p.i3, p.alpha0 = n, 1, float(i3), float(alpha0)
+    L = np.asarray(prior_chol, dtype=np.float64)
+    for i in range(n):
+        p.r[i] = float(r[i])
+        p.theta[i] = float(theta[i])
+        for j in range(i + 1):
+            p.prior_chol[i * MC_MAX_N + j] = float(L[i, j])
+    return p
+
+
+def problem_point_mass(r, theta, i3: float, alpha0: float = 0.025) -> mc_problem:
+    p = mc_problem()
+    n = len(r)
+    p.n, p.has_prior_chol, p.i3, p.alpha0 = n, 0, float(i3), float(alpha0)
+    for i in range(n):
+        p.r[i], p.theta[i], p.sigma[i] = float(r[i]), float(theta[i]), 0.0
+    return p
+
+
+def _problem_array(problems):
+    arr = (mc_problem * len(problems))()
+    for i, p in enumerate(problems):
+        arr[i] = p
+    return arr
+
+
+def fwer(problem: mc_problem, alpha, device: int = 0) -> np.ndarray:
+    a = np.ascontiguousarray(np.atleast_2d(alpha), dtype=np.float64)
+    out = np.zeros(a.shape[0])
+    _check(lib().mc_fwer(ctypes.byref(problem), _dp(a), a.shape[0], _dp(out), device))
+    return out
+
+
+def candidates(problems, m: int = 64, n3: int = 0, seed: int = 0, device: int = 0):
+    """Row a1: the alpha grid with alpha_n solved on the GPU and the seeded N3 subset.
+    Returns (alpha[D, n], problem_of_design[D])."""
+    arr = _problem_array(problems)
+    n = problems[0].n
+    need = ctypes.c_int64(0)
+    st = lib().mc_candidates(arr, len(problems), m, n3, seed, None, None, 0, ctypes.byref(need), device)
+    if st not in (0, 1):
+        _check(st)
+    cap = max(int(need.value), 1)
+    A = np.zeros((cap, n))
+    pod = np.zeros(cap, dtype=np.int32)
+    _check(lib().mc_candidates(arr, len(problems), m, n3, seed, _dp(A), pod.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                               cap, ctypes.byref(need), device))
+    D = int(need.value)
+    return A[:D], pod[:D]
+
+
+def philox_dump(seed: int, design, word, stream=None):
+    """K3: Philox words for (design, word-index) pairs (device tensors in, device tensor out)."""
+    torch = _torch()
+    design = design.to(torch.int32).contiguous()
+    word = word.to(torch.int64).contiguous()
+    out = torch.empty(design.numel(), dtype=torch.int32, device=design.device)
+    _check(lib().mc_philox_dump(seed, design.data_ptr(), word.data_ptr(), design.numel(), out.data_ptr(), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------------------------------
+
+class Design:
+    """A device design table (mc_design_init) and the hot-path calls on it."""
+
+    def __init__(self, problems, alpha, problem_of_design, seed: int, estimator: int = EST_COND, device: int = 0):
+        torch = _torch()
+        self.device = device
+        self.problems = list(problems)
+        self.n = self.problems[0].n
+        a = np.ascontiguousarray(alpha, dtype=np.float64).reshape(-1, self.n)
+        pod = np.ascontiguousarray(problem_of_design, dtype=np.int32)
+        self.alpha = a
+        self.pod = pod
+        self.D = a.shape[0]
+        self.seed = int(seed)
+        self.estimator = int(estimator)
+        arr = _problem_array(self.problems)
+        ctx = ctypes.c_void_p()
+        torch.cuda.set_device(device)
+        _check(lib().mc_design_init(ctypes.byref(ctx), arr, len(self.problems), _dp(a),
+                                    pod.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), self.D, self.seed,
+                                    self.estimator, device))
+        self._ctx = ctx
+        self.n_probs = len(self.problems)
+
+    def close(self):
+        if getattr(self, "_ctx", None) is not None and self._ctx.value:
+            lib().mc_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def words_per_draw(self) -> int:
+        return int(lib().mc_words_per_draw(self._ctx))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().mc_kernel_launches(self._ctx))
+
+    def set_launch(self, block_threads: int = 0, grid_blocks: int = 0):
+        _check(lib().mc_set_launch(self._ctx, block_threads, grid_blocks))
+
+    def new_sums(self):
+        torch = _torch()
+        return torch.zeros((self.D, 2), dtype=torch.int64, device=f"cuda:{self.device}")
+
+    def evaluate(self, sums, sample_begin: int, sample_count: int, design_begin: int = 0, design_count=None,
+                 stream=None):
+        """Rows a2-a6: accumulate the integer sums of samples [begin, begin+count) into `sums`."""
+        if design_count is None:
+            design_count = self.D - design_begin
+        assert sums.is_cuda and sums.dtype.is_floating_point is False and sums.numel() == 2 * self.D
+        _check(lib().mc_evaluate_grid(self._ctx, design_begin, design_count, sample_begin, sample_count,
+                                      _stream(stream), sums.data_ptr()))
+        return sums
+
+    def finalize(self, sums, total_samples: int, stream=None):
+        """Row a8: per-design mean and per-draw variance (fp64 tensors)."""
+        torch = _torch()
+        mean = torch.empty(self.D, dtype=torch.float64, device=sums.device)
+        var = torch.empty(self.D, dtype=torch.float64, device=sums.device)
+        _check(lib().mc_finalize(self._ctx, sums.data_ptr(), total_samples, mean.data_ptr(), var.data_ptr(),
+                                 _stream(stream)))
+        return mean, var
+
+    def smooth_plan(self, fit_mask=None, stream=None):
+        m = None
+        if fit_mask is not None:
+            m = np.ascontiguousarray(fit_mask, dtype=np.uint8)
+            assert m.size == self.D
+        _check(lib().mc_smooth_plan(self._ctx, None if m is None else m.ctypes.data_as(ctypes.c_void_p),
+                                    _stream(stream)))
+        self._mask_ref = m
+
+    def smooth(self, values, lam: float = -1.0, stream=None):
+        """Row a9: TPS-smoothed values and the lambda used per problem."""
+        torch = _torch()
+        out = torch.empty_like(values)
+        lam_used = torch.empty(self.n_probs, dtype=torch.float64, device=values.device)
+        _check(lib().mc_smooth(self._ctx, values.data_ptr(), float(lam), out.data_ptr(), lam_used.data_ptr(),
+                               _stream(stream)))
+        return out, lam_used
+
+    def argmax(self, values, with_host: bool = True, stream=None):
+        """Row a10: per-problem argmax (device) and, if with_host, the overall (index, value)."""
+        torch = _torch()
+        idx = torch.empty(self.n_probs, dtype=torch.int64, device=values.device)
+        val = torch.empty(self.n_probs, dtype=torch.float64, device=values.device)
+        bi = ctypes.c_int64(-1)
+        bv = ctypes.c_double(float("nan"))
+        _check(lib().mc_argmax(self._ctx, values.data_ptr(), idx.data_ptr(), val.data_ptr(),
+                               ctypes.byref(bi) if with_host else None, ctypes.byref(bv) if with_host else None,
+                               _stream(stream)))
+        return idx, val, (int(bi.value), float(bv.value)) if with_host else None
+
+    def draw_dump(self, design, sample, stream=None):
+        torch = _torch()
+        design = design.to(torch.int64).contiguous()
+        sample = sample.to(torch.int64).contiguous()
+        stride = int(lib().mc_draw_dump_stride(self._ctx))
+        out = torch.empty((design.numel(), stride), dtype=torch.float32, device=design.device)
+        _check(lib().mc_draw_dump(self._ctx, design.data_ptr(), sample.data_ptr(), design.numel(), out.data_ptr(),
+                                  _stream(stream)))
+        return out
+
+
+# ------------------------------------------------------------------------------------------
+# Multi-GPU: samples shard by rank; one all_reduce of the int64 sums (row a7).
+
+def shard_range(total: int, rank: int, world: int, align: int = 64):
+    """Rank `rank`'s sample range [begin, begin + count) of `total` samples: contiguous blocks
+    in multiples of `align` (the last rank takes the remainder)."""
+    per = (total // world) // align * align
+    begin = rank * per
+    count = per if rank < world - 1 else total - per * (world - 1)
+    return begin, count
+
+
+def allreduce_sums(sums):
+    """Row a7: the single cross-GPU combine.  Integer SUM => bit-identical for any world size."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    return sums
+
+
+@dataclass
+class Result:
+    mean: object
+    var: object
+    smoothed: object
+    lam_used: object
+    idx: object
+    val: object
+    best: tuple
+
+
+def evaluate_design_objective(design: Design, total_samples: int, lam: float = -1.0, smooth: bool = True,
+                              rank: int = 0, world: int = 1, stream=None) -> Result:
+    """One pass of the whole hot path (rows a2-a10) for this rank's sample shard."""
+    sums = design.new_sums()
+    b, c = shard_range(total_samples, rank, world)
+    design.evaluate(sums, b, c, stream=stream)
+    allreduce_sums(sums)
+    mean, var = design.finalize(sums, total_samples, stream=stream)
+    if smooth:
+        sm, lam_used = design.smooth(mean, lam, stream=stream)
+    else:
+        sm, lam_used = mean, None
+    idx, val, best = design.argmax(sm, stream=stream)
+    return Result(mean, var, sm, lam_used, idx, val, best)

@@ -1,0 +1,148 @@
+"""GPU parity of design prep (row a1: FWER, alpha grid, N3 subset), smoothing (a9) and argmax (a10)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2005_10494_b200 import workloads as W
+from tests.helpers import lib_problem, oracle_problem, slice_designs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def mc(torch):
+    from paper_2005_10494_b200 import build, mc as m
+    build.build()
+    return m
+
+
+@pytest.mark.parametrize("r", [[1.0], [1.0, 0.3], [1.0, 0.45, 0.15], [1.0, 0.95, 0.9], [1.0, 0.8, 0.6, 0.4, 0.2]])
+def test_fwer_matches_oracle(O, mc, r):
+    n = len(r)
+    spec_p = mc.problem_formula10(r, [0.25] * n, 211.0)
+    rng = np.random.default_rng(n)
+    A = rng.uniform(0, 0.012, size=(12, n))
+    A[0, -1] = 0.0            # alpha = 0 -> z = +inf
+    got = mc.fwer(spec_p, A)
+    ref = np.array([O.fwer(r, a) for a in A])
+    assert np.allclose(got, ref, rtol=0, atol=2e-12 if n <= 3 else 2e-8)
+
+
+def test_candidates_grid_matches_oracle(O, mc):
+    """m = 12 grid of the C2 slice problem: feasibility identical, alpha_3 within 1e-11."""
+    spec = W.c2_slice()
+    m = 12
+    A, pod = mc.candidates([lib_problem(mc, spec)], m=m, n3=0, seed=W.SEED)
+    Ao, ok = O.alpha_grid(spec.r, spec.alpha0, m, 1e-14)
+    ref = Ao[ok]
+    # borderline points (FWER(.., 0) within 1e-10 of alpha0) may legitimately differ
+    assert len(A) == len(ref)
+    assert np.allclose(A[:, :2], ref[:, :2], atol=0)
+    assert np.allclose(A[:, 2], ref[:, 2], atol=1e-11)
+    assert np.all(pod == 0)
+    for a in A[:: max(1, len(A) // 10)]:
+        assert O.fwer(spec.r, a) == pytest.approx(spec.alpha0, abs=1e-11)
+
+
+def test_candidates_m64_sampled_and_subset(O, mc):
+    """Full m = 64 slice grid on the GPU: 40 sampled grid points against the oracle's solve, and the
+    seeded N3 subset equal to the oracle's Fisher-Yates on the same valid list."""
+    spec = W.c2_slice()
+    Aall, _ = mc.candidates([lib_problem(mc, spec)], m=64, n3=0, seed=W.SEED)
+    V = len(Aall)
+    assert 2000 < V < 4096
+    rng = np.random.default_rng(2)
+    for i in rng.choice(V, 40, replace=False):
+        a3 = O.solve_alpha_n(spec.r, spec.alpha0, Aall[i, :2], 1e-14)
+        assert a3 is not None and abs(a3 - Aall[i, 2]) < 1e-11
+    # grid points not in the list are infeasible for the oracle too (sampled)
+    have = {(round(a[0] / spec.alpha0 * 64 - 0.5), round(a[1] / spec.alpha0 * 64 - 0.5)) for a in Aall}
+    missing = [(i, j) for i in range(64) for j in range(64) if (i, j) not in have]
+    for i, j in [missing[k] for k in rng.choice(len(missing), min(20, len(missing)), replace=False)]:
+        a = [(i + 0.5) * spec.alpha0 / 64, (j + 0.5) * spec.alpha0 / 64]
+        assert O.solve_alpha_n(spec.r, spec.alpha0, a, 1e-10) is None
+    A2, _ = mc.candidates([lib_problem(mc, spec)], m=64, n3=W.N3, seed=W.SEED)
+    sel = O.subset(V, W.N3, W.SEED)
+    assert np.array_equal(A2, Aall[sel])
+
+
+def test_candidates_batch_problem_seeds(O, mc):
+    specs = [W.ProblemSpec(r=(1.0, 0.6, 0.2), scenario="c", i3=211.0),
+             W.ProblemSpec(r=(1.0, 0.3, 0.1), scenario="b", i3=211.0)]
+    A, pod = mc.candidates([lib_problem(mc, s) for s in specs], m=20, n3=150, seed=99)
+    assert np.array_equal(np.bincount(pod), [150, 150])
+    for k, s in enumerate(specs):
+        Ak, _ = mc.candidates([lib_problem(mc, s)], m=20, n3=0, seed=0)
+        assert np.array_equal(A[pod == k], Ak[O.subset(len(Ak), 150, 99 + k)])
+
+
+def test_candidates_infeasible_n3(mc):
+    with pytest.raises(mc.McError) as e:
+        mc.candidates([lib_problem(mc, W.c2_slice())], m=8, n3=1000, seed=1)
+    assert e.value.status == 3
+
+
+def _noisy_surface(O, m=20, seed=0):
+    spec, alpha = slice_designs(O, m=m, count=None)
+    x = alpha[:, :2] / spec.alpha0
+    f = 0.95 + 0.02 * np.sin(3 * x[:, 0]) * np.cos(2 * x[:, 1]) - 0.01 * x[:, 0] ** 2
+    y = f + 1e-3 * np.random.default_rng(seed).normal(size=len(f))
+    return spec, alpha, x, f, y
+
+
+@pytest.mark.parametrize("lam", [-1.0, 1e-6, 1e-3, 0.0])
+def test_tps_smoothing_matches_oracle(O, mc, torch, lam):
+    spec, alpha, x, f, y = _noisy_surface(O)
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(len(alpha), dtype=np.int32), seed=1)
+    vals = torch.tensor(y, dtype=torch.float64, device="cuda")
+    sm, lam_used = dsg.smooth(vals, lam)
+    ref, lam_ref = O.tps_smooth(x, y, lam)
+    if lam >= 0:
+        assert lam_used.item() == lam
+    else:
+        # same grid point chosen (or GCV values tied to 1e-9)
+        if lam_used.item() != pytest.approx(lam_ref, rel=1e-9):
+            g1 = O.gcv_score(x, y, lam_used.item())
+            g2 = O.gcv_score(x, y, lam_ref)
+            assert g1 == pytest.approx(g2, rel=1e-9)
+    assert np.allclose(sm.cpu().numpy(), ref, rtol=0, atol=1e-9)
+
+
+def test_tps_mask_and_passthrough(O, mc, torch):
+    spec, alpha, x, f, y = _noisy_surface(O, m=16, seed=1)
+    mask = (alpha[:, 2] >= spec.alpha0 / 25).astype(np.uint8)      # ridge band excluded from the fit
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(len(alpha), dtype=np.int32), seed=1)
+    dsg.smooth_plan(mask)
+    vals = torch.tensor(y, dtype=torch.float64, device="cuda")
+    sm, _ = dsg.smooth(vals, 1e-5)
+    sm = sm.cpu().numpy()
+    keep = mask.astype(bool)
+    ref, _ = O.tps_smooth(x[keep], y[keep], 1e-5)
+    assert np.allclose(sm[keep], ref, atol=1e-9)
+    assert np.array_equal(sm[~keep], y[~keep])
+
+
+def test_segmented_argmax_matches_oracle(O, mc, torch):
+    specs = [W.ProblemSpec(r=(1.0, 0.6, 0.2), scenario="c", i3=211.0)] * 3
+    rng = np.random.default_rng(3)
+    sizes = [5, 1, 300]
+    alpha = np.concatenate([np.tile([[0.01, 0.01, 0.001]], (s, 1)) for s in sizes])
+    pod = np.repeat(np.arange(3), sizes).astype(np.int32)
+    dsg = mc.Design([lib_problem(mc, s) for s in specs], alpha, pod, seed=1)
+    v = rng.normal(size=len(alpha))
+    v[2] = v[3] = 10.0          # tie inside problem 0 -> lowest index
+    v[100] = np.nan             # NaN never wins
+    idx, val, (bi, bv) = dsg.argmax(torch.tensor(v, device="cuda"))
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    for k in range(3):
+        seg = np.where(np.isnan(v[off[k]:off[k + 1]]), -np.inf, v[off[k]:off[k + 1]])
+        assert idx[k].item() == off[k] + O.argmax(seg)
+    assert bi == 2 and bv == 10.0
