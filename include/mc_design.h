@@ -109,6 +109,12 @@ mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs,
                          const double* alpha_host, const int32_t* problem_of_design_host,
                          int64_t D, uint64_t seed, int32_t estimator, int32_t cuda_device);
 
+/* Replaces the design table's alpha (same D, n and problem_of_design) from the HOST buffer
+ * alpha_host[D*n] (pinned memory makes the copy asynchronous): H2D copy on `cuda_stream` and an fp64
+ * device kernel recomputing zc.  Host-validated like mc_design_init.  The smoothing plan is kept iff
+ * the new alpha equals the previous table (the TPS sites are unchanged), else it is invalidated. */
+mc_status mc_design_upload(mc_ctx* ctx, const double* alpha_host, void* cuda_stream);
+
 /* Launch shape of the fused kernel (results do not depend on it): threads per block (multiple of
  * 32 in [32, 256]; 0 = default 256) and grid blocks (>= 0; 0 = #SMs x max resident blocks). */
 mc_status mc_set_launch(mc_ctx* ctx, int32_t block_threads, int32_t grid_blocks);
@@ -176,7 +182,7 @@ mc_status mc_draw_dump(mc_ctx* ctx, const int64_t* design_dev, const uint64_t* s
                        int64_t count, float* out_dev, void* cuda_stream);
 int32_t mc_draw_dump_stride(const mc_ctx* ctx);
 
-/* Number of fused-kernel launches issued by this ctx since creation (bench gpu_launches). */
+/* Number of CUDA kernel launches issued by this ctx's calls since creation (bench gpu_launches). */
 int64_t mc_kernel_launches(const mc_ctx* ctx);
 
 const char* mc_last_error(void);

@@ -98,8 +98,17 @@ static mc_status validate_problem(const mc_problem& p, int idx) {
   return MC_OK;
 }
 
-// Per-problem device record (fp32): M = diag(c) L_p packed, rho, s, 1/s (Formula 1/3/10, A.1).
-static void problem_record(const mc_problem& p, float* rec) {
+constexpr double BM_K = 1.17741002251547469;   // sqrt(2 ln 2), see mc_device.cuh
+
+// Row scale of b folded into the record and the thresholds (mc_device.cuh ProbRegs).
+static double row_scale(const mc_problem& p, int est, int i) {
+  if (est == MC_EST_IND) return 1.0 / BM_K;
+  return i == 0 ? 1.0 : 1.0 / std::sqrt(1.0 - p.r[i] / p.r[i - 1]);
+}
+
+// Per-problem device record (fp32): M = diag(c) L_p packed with the folded scales, rho, s, rho/s,
+// row scales (Formula 1/3/10, A.1).
+static void problem_record(const mc_problem& p, int est, float* rec) {
   const int n = p.n;
   double rho[MC_MAX_N] = {0}, sd[MC_MAX_N] = {0};
   for (int i = 0; i + 1 < n; ++i) {
@@ -120,12 +129,15 @@ static void problem_record(const mc_problem& p, float* rec) {
   std::fill(rec, rec + PROB_STRIDE, 0.0f);
   for (int i = 0; i < n; ++i) {
     const double c = std::sqrt(p.r[i] * p.i3);
-    for (int j = 0; j <= i; ++j) rec[OFF_M + i * (i + 1) / 2 + j] = (float)(c * Lp[i][j]);
+    // the kernel draws eps / BM_K: M carries BM_K times the row scale (= 1 for IND)
+    const double f = est == MC_EST_IND ? 1.0 : BM_K * row_scale(p, est, i);
+    for (int j = 0; j <= i; ++j) rec[OFF_M + i * (i + 1) / 2 + j] = (float)(f * c * Lp[i][j]);
+    rec[OFF_BSC + i] = (float)row_scale(p, est, i);
   }
   for (int i = 0; i + 1 < n; ++i) {
     rec[OFF_RHO + i] = (float)rho[i];
     rec[OFF_SD + i] = (float)sd[i];
-    rec[OFF_ISD + i] = (float)(1.0 / sd[i]);
+    rec[OFF_RIS + i] = (float)(rho[i] / sd[i]);
   }
 }
 
@@ -234,33 +246,62 @@ mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs,
   c->prob_begin = begin;
 
   std::vector<float> rec((size_t)n_probs * PROB_STRIDE);
-  for (int k = 0; k < n_probs; ++k) problem_record(probs[k], &rec[(size_t)k * PROB_STRIDE]);
-  std::vector<float> zc((size_t)std::max<int64_t>(D, 1) * n);
-  for (int64_t d = 0; d < D; ++d) {
-    const mc_problem& p = probs[pod[d]];
+  for (int k = 0; k < n_probs; ++k) problem_record(probs[k], estimator, &rec[(size_t)k * PROB_STRIDE]);
+  std::vector<double> ctheta((size_t)n_probs * n * 2);
+  for (int k = 0; k < n_probs; ++k)
     for (int i = 0; i < n; ++i) {
-      const double z = threshold(alpha[d * n + i]);
-      const double v = z - std::sqrt(p.r[i] * p.i3) * p.theta[i];   // z_i - c_i theta_i
-      zc[d * n + i] = (float)v;
+      ctheta[((size_t)k * n + i) * 2] = std::sqrt(probs[k].r[i] * probs[k].i3) * probs[k].theta[i];
+      ctheta[((size_t)k * n + i) * 2 + 1] = row_scale(probs[k], estimator, i);
     }
-  }
   auto fail = [&](cudaError_t e, const char* w) { mc_status s = cuda_fail(e, w); mc_destroy(c); return s; };
   cudaError_t e;
   if ((e = cudaMalloc(&c->d_prob, rec.size() * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc prob");
-  if ((e = cudaMalloc(&c->d_zc, zc.size() * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc zc");
+  const size_t Dn = (size_t)std::max<int64_t>(D, 1) * n;
+  if ((e = cudaMalloc(&c->d_zc, Dn * sizeof(float))) != cudaSuccess) return fail(e, "cudaMalloc zc");
+  if ((e = cudaMalloc(&c->d_alpha, Dn * sizeof(double))) != cudaSuccess) return fail(e, "cudaMalloc alpha");
+  if ((e = cudaMalloc(&c->d_ctheta, ctheta.size() * sizeof(double))) != cudaSuccess) return fail(e, "cudaMalloc ctheta");
   if ((e = cudaMalloc(&c->d_pod, std::max<int64_t>(D, 1) * sizeof(int32_t))) != cudaSuccess) return fail(e, "cudaMalloc pod");
   if ((e = cudaMalloc(&c->d_prob_begin, begin.size() * sizeof(int64_t))) != cudaSuccess) return fail(e, "cudaMalloc begin");
   if ((e = cudaMemcpy(c->d_prob, rec.data(), rec.size() * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
     return fail(e, "upload prob");
-  if ((e = cudaMemcpy(c->d_zc, zc.data(), zc.size() * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
-    return fail(e, "upload zc");
+  if (D > 0 && (e = cudaMemcpy(c->d_alpha, alpha, (size_t)D * n * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e, "upload alpha");
+  if ((e = cudaMemcpy(c->d_ctheta, ctheta.data(), ctheta.size() * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e, "upload ctheta");
   if (D > 0 && (e = cudaMemcpy(c->d_pod, pod, D * sizeof(int32_t), cudaMemcpyHostToDevice)) != cudaSuccess)
     return fail(e, "upload pod");
   if ((e = cudaMemcpy(c->d_prob_begin, begin.data(), begin.size() * sizeof(int64_t), cudaMemcpyHostToDevice)) !=
       cudaSuccess)
     return fail(e, "upload begin");
+  {
+    mc_status s = launch_zc(c, nullptr);
+    if (s != MC_OK) { mc_destroy(c); return s; }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e, "k_zc");
+  }
+  c->launches = 0;
   *ctx = c;
   return MC_OK;
+}
+
+mc_status mc_design_upload(mc_ctx* c, const double* alpha, void* stream) {
+  if (!c || (c->D > 0 && !alpha)) { set_error("mc_design_upload: null pointer"); return MC_ERR_INVALID; }
+  const int n = c->n;
+  for (int64_t d = 0; d < c->D; ++d) {
+    const double a0 = c->probs[c->pod[d]].alpha0;
+    for (int i = 0; i < n; ++i) {
+      const double a = alpha[d * n + i];
+      if (!(a >= 0.0 && a <= a0)) { set_error("mc_design_upload: alpha outside [0, alpha0] (P:221)"); return MC_ERR_INVALID; }
+    }
+  }
+  if (std::memcmp(c->alpha.data(), alpha, sizeof(double) * (size_t)c->D * n) != 0) {
+    std::memcpy(c->alpha.data(), alpha, sizeof(double) * (size_t)c->D * n);
+    c->plan_built = false;   // TPS sites changed: the plan is rebuilt on the next mc_smooth
+  }
+  MC_CUDA(cudaSetDevice(c->device));
+  if (c->D == 0) return MC_OK;
+  MC_CUDA(cudaMemcpyAsync(c->d_alpha, alpha, sizeof(double) * (size_t)c->D * n, cudaMemcpyHostToDevice,
+                          (cudaStream_t)stream));
+  return launch_zc(c, (cudaStream_t)stream);
 }
 
 mc_status mc_set_launch(mc_ctx* c, int32_t threads, int32_t grid) {
@@ -286,6 +327,8 @@ void mc_destroy(mc_ctx* c) {
   cudaFree(c->d_tps_scratch);
   cudaFree(c->d_prob);
   cudaFree(c->d_zc);
+  cudaFree(c->d_alpha);
+  cudaFree(c->d_ctheta);
   cudaFree(c->d_pod);
   cudaFree(c->d_prob_begin);
   delete c;

@@ -30,10 +30,19 @@ struct Geo {
 // Philox4x32-10 (Salmon et al., SC'11).  Counter (q_lo, q_hi, design, 0), key (seed_lo, seed_hi).
 struct Key { uint32_t k0, k1; };
 
+// 32x32 -> 64-bit product as ONE IMAD.WIDE.U32 (ptxas otherwise often splits it into IMAD.HI + IMAD).
+__device__ __forceinline__ void mulhilo(uint32_t a, uint32_t m, uint32_t& hi, uint32_t& lo) {
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(m));
+  lo = (uint32_t)p;
+  hi = (uint32_t)(p >> 32);
+}
+
 __device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
                                              uint32_t k0, uint32_t k1) {
-  const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
-  const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+  uint32_t lo0, hi0, lo1, hi1;
+  mulhilo(c0, 0xD2511F53u, hi0, lo0);
+  mulhilo(c2, 0xCD9E8D57u, hi1, lo1);
   c0 = hi1 ^ c1 ^ k0;
   c1 = lo1;
   c2 = hi0 ^ c3 ^ k1;
@@ -46,10 +55,12 @@ __device__ __forceinline__ void philox_block(uint64_t q, uint32_t lo1d, uint32_t
                                              uint32_t out[4]) {
   const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32);
   // round 1 with c2 = design, c3 = 0
+  uint32_t hq, lq;
+  mulhilo(q0, 0xD2511F53u, hq, lq);
   uint32_t c0 = hi1d ^ q1 ^ key.k0;
   uint32_t c1 = lo1d;
-  uint32_t c2 = __umulhi(0xD2511F53u, q0) ^ key.k1;
-  uint32_t c3 = 0xD2511F53u * q0;
+  uint32_t c2 = hq ^ key.k1;
+  uint32_t c3 = lq;
   uint32_t k0 = key.k0, k1 = key.k1;
 #pragma unroll
   for (int r = 1; r < 10; ++r) {
@@ -76,8 +87,24 @@ __device__ __forceinline__ float sqrt_approx(float x) { float y; asm("sqrt.appro
 __device__ __forceinline__ float sin_approx(float x) { float y; asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float cos_approx(float x) { float y; asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
-// 1 + k 2^-23 in [1, 2) from the low 23 bits k of a Philox word (one LOP3): DESIGN.md §2.3.
+// 1 + k 2^-23 in [1, 2) from the low 23 bits k of a Philox word: DESIGN.md §2.3.
 __device__ __forceinline__ float word_to_f12(uint32_t w) { return __uint_as_float((w & 0x007FFFFFu) | 0x3F800000u); }
+// Same as one LOP3 ((w & 0x7FFFFF) | one): `one` = 0x3F800000 held in a register by the caller
+// (ptxas cannot encode two immediates in one LOP3).
+__device__ __forceinline__ float word_to_f12(uint32_t w, uint32_t one) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, 0x007FFFFF, %2, 0xEA;" : "=r"(r) : "r"(w), "r"(one));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t one_bits_reg() {
+  uint32_t r;
+  asm volatile("mov.b32 %0, 0x3F800000;" : "=r"(r));
+  return r;
+}
+
+// Box-Muller scale: R = sqrt(-2 ln u) = BM_K sqrt(-log2 u), BM_K = sqrt(2 ln 2).  The kernel draws the
+// scaled normals eps / BM_K and folds BM_K into the per-problem factors (see problem_record()).
+constexpr float BM_K = 1.17741002251547469f;
 
 // Box-Muller pair from words (wr, wa): R = sqrt(-2 ln u_r), angle 2 pi u_a.
 // u_r = 2 - f(wr) in (0,1]; the angle is evaluated as 2 pi (u_a - 1/2) in [-pi, pi) (MUFU's
@@ -87,6 +114,16 @@ __device__ __forceinline__ void box_muller(uint32_t wr, uint32_t wa, float& n0, 
   const float t = fmaxf(-1.38629436112f * lg2_approx(ur), 0.0f);   // -2 ln u_r
   const float mr = -sqrt_approx(t);
   const float x = (word_to_f12(wa) - 1.5f) * 6.28318530718f;
+  n0 = mr * cos_approx(x);
+  n1 = mr * sin_approx(x);
+}
+
+// The kernel's Box-Muller: returns (n0, n1) / BM_K.  sqrt(|log2 u_r|) replaces the clamp at 0 (log2 of
+// u_r <= 1 can come back ~1e-7 positive from MUFU.LG2); the angle 2 pi (u_a - 1/2) is one FFMA.
+__device__ __forceinline__ void box_muller_scaled(uint32_t wr, uint32_t wa, uint32_t one, float& n0, float& n1) {
+  const float ur = 2.0f - word_to_f12(wr, one);
+  const float mr = -sqrt_approx(fabsf(lg2_approx(ur)));
+  const float x = fmaf(word_to_f12(wa, one), 6.28318530718f, -9.42477796077f);
   n0 = mr * cos_approx(x);
   n1 = mr * sin_approx(x);
 }
@@ -164,22 +201,70 @@ __device__ __forceinline__ float normal_quantile(float p, float pc) {
   return 1.41421356237f * g * (p - pc);
 }
 
+// normal_quantile() with sqrt(2) folded into the polynomial coefficients (one FMUL less).
+__device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
+  constexpr double S2 = 1.4142135623730950488;
+  const float w = -0.69314718056f * (lg2_approx(fmaxf(p * pc, 1.0e-38f)) + 2.0f);
+  float g;
+  if (w < 5.0f) {
+    const float ww = w - 2.5f;
+    g = (float)(2.81022636e-08 * S2);
+    g = fmaf(g, ww, (float)(3.43273939e-07 * S2));
+    g = fmaf(g, ww, (float)(-3.5233877e-06 * S2));
+    g = fmaf(g, ww, (float)(-4.39150654e-06 * S2));
+    g = fmaf(g, ww, (float)(0.00021858087 * S2));
+    g = fmaf(g, ww, (float)(-0.00125372503 * S2));
+    g = fmaf(g, ww, (float)(-0.00417768164 * S2));
+    g = fmaf(g, ww, (float)(0.246640727 * S2));
+    g = fmaf(g, ww, (float)(1.50140941 * S2));
+  } else {
+    const float sw = sqrt_approx(fminf(w, 88.0f));
+    if (w < 16.0f) {
+      const float ww = sw - 3.0f;
+      g = (float)(-0.000200214257 * S2);
+      g = fmaf(g, ww, (float)(0.000100950558 * S2));
+      g = fmaf(g, ww, (float)(0.00134934322 * S2));
+      g = fmaf(g, ww, (float)(-0.00367342844 * S2));
+      g = fmaf(g, ww, (float)(0.00573950773 * S2));
+      g = fmaf(g, ww, (float)(-0.0076224613 * S2));
+      g = fmaf(g, ww, (float)(0.00943887047 * S2));
+      g = fmaf(g, ww, (float)(1.00167406 * S2));
+      g = fmaf(g, ww, (float)(2.83297682 * S2));
+    } else {
+      const float ww = sw - 6.0f;
+      g = (float)(7.926354328446905e-07 * S2);
+      g = fmaf(g, ww, (float)(-6.932396900083404e-06 * S2));
+      g = fmaf(g, ww, (float)(2.5214179913746193e-05 * S2));
+      g = fmaf(g, ww, (float)(-3.964155257563107e-05 * S2));
+      g = fmaf(g, ww, (float)(-0.0004801170143764466 * S2));
+      g = fmaf(g, ww, (float)(1.0096029043197632 * S2));
+      g = fmaf(g, ww, (float)(5.859915256500244 * S2));
+    }
+  }
+  return g * (p - pc);
+}
+
 // ---------------------------------------------------------------------------------------------
-// Per-problem parameters in registers (loaded once per tile; uniform across the block).
+// Per-problem parameters in registers (loaded once per tile; uniform across the block).  The device
+// record folds constant factors (mc_api.cu problem_record()):
+//   COND: row i of M and zc carry bs_i = (i == 0 ? 1 : 1/s_{i-1}), M also BM_K, so the kernel's
+//         b'_i = b_i bs_i and the SOV stage argument is a_i = b'_i - (rho_{i-1}/s_{i-1}) x_{i-1}.
+//   IND:  zc carries 1/BM_K and M is unscaled: b' = b / BM_K compared with X' = X / BM_K.
 template <int N>
 struct ProbRegs {
-  float M[N * (N + 1) / 2];   // M = diag(c) L_p, packed lower triangular (row i: M[i(i+1)/2 + j])
-  float rho[N > 1 ? N - 1 : 1], sd[N > 1 ? N - 1 : 1], isd[N > 1 ? N - 1 : 1];
+  float M[N * (N + 1) / 2];   // packed lower triangular (row i: M[i(i+1)/2 + j])
+  float rho[N > 1 ? N - 1 : 1], sd[N > 1 ? N - 1 : 1], ris[N > 1 ? N - 1 : 1];   // rho, s, rho/s
 };
 
-// One draw from its U words w[0..U): returns u in [0,1].  If DBG, writes the normals, b and u.
+// One draw from its U words w[0..U): returns u in [0,1].  If DBG, writes the (unscaled) normals,
+// b and u; bsc[i] (the row scales) and BM_K undo the folding for the dump.
 template <int N, int EST, bool DBG>
-__device__ __forceinline__ float draw_utility(const uint32_t* w, const float* zc, const ProbRegs<N>& pr,
-                                              float* dbg = nullptr) {
+__device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, const float* zc, const ProbRegs<N>& pr,
+                                              float* dbg = nullptr, const float* bsc = nullptr) {
   using G = Geo<N, EST>;
   float nrm[2 * G::NPAIR];
 #pragma unroll
-  for (int j = 0; j < G::NPAIR; ++j) box_muller(w[2 * j], w[2 * j + 1], nrm[2 * j], nrm[2 * j + 1]);
+  for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(w[2 * j], w[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
   // b_i = z_i - c_i Delta_i = (z_i - c_i theta_i) - sum_{j<=i} (c_i L_p,ij) eps_j   (Formulas 3-5, 10)
   float b[N];
 #pragma unroll
@@ -208,27 +293,26 @@ __device__ __forceinline__ float draw_utility(const uint32_t* w, const float* zc
     u = q;
     float x = 0.0f;
     if constexpr (N > 1) {
-      const float v = word_to_f12(w[VB]) - 0.99999994039535522f;      // (k + 1/2) 2^-23
+      const float v = word_to_f12(w[VB], one) - 0.99999994039535522f;  // (k + 1/2) 2^-23
       const float vc = 1.0f - v;                                       // exact
-      x = normal_quantile(v * e, fmaf(v, q, vc));
+      x = normal_quantile_fast(v * e, fmaf(v, q, vc));
     }
 #pragma unroll
     for (int i = 1; i < N; ++i) {
-      const float m = pr.rho[i - 1] * x;
-      normal_tail((b[i] - m) * pr.isd[i - 1], q, e);
+      normal_tail(fmaf(-pr.ris[i - 1], x, b[i]), q, e);
       u = fmaf(1.0f - u, q, u);
       if (i + 1 < N) {
-        const float v = word_to_f12(w[VB + i]) - 0.99999994039535522f;
+        const float v = word_to_f12(w[VB + i], one) - 0.99999994039535522f;
         const float vc = 1.0f - v;
-        x = fmaf(pr.sd[i - 1], normal_quantile(v * e, fmaf(v, q, vc)), m);
+        x = fmaf(pr.sd[i - 1], normal_quantile_fast(v * e, fmaf(v, q, vc)), pr.rho[i - 1] * x);
       }
     }
   }
   if constexpr (DBG) {
 #pragma unroll
-    for (int k = 0; k < G::NNORM; ++k) dbg[k] = nrm[k];
+    for (int k = 0; k < G::NNORM; ++k) dbg[k] = nrm[k] * BM_K;
 #pragma unroll
-    for (int i = 0; i < N; ++i) dbg[G::NNORM + i] = b[i];
+    for (int i = 0; i < N; ++i) dbg[G::NNORM + i] = b[i] / bsc[i];
     dbg[G::NNORM + N] = u;
   }
   return u;

@@ -10,11 +10,12 @@
 
 namespace mci {
 
-constexpr int PROB_STRIDE = 96;          // floats per device problem record
-constexpr int OFF_M = 0;                 // packed M = diag(c) L_p (55 floats for n = 10)
+constexpr int PROB_STRIDE = 112;         // floats per device problem record
+constexpr int OFF_M = 0;                 // packed M = diag(c) L_p with the folded row scales (55 floats for n = 10)
 constexpr int OFF_RHO = 56;              // rho_i = sqrt(r_{i+1}/r_i)
 constexpr int OFF_SD = 66;               // s_i = sqrt(1 - rho_i^2)
-constexpr int OFF_ISD = 76;              // 1/s_i
+constexpr int OFF_RIS = 76;              // rho_i / s_i
+constexpr int OFF_BSC = 86;              // row scale of b' = b * bsc (dump only)
 constexpr int SAMPLES_PER_THREAD = 64;   // per-thread sample run inside a tile
 constexpr int MAX_BLOCK = 256;           // fused kernel __launch_bounds__
 
@@ -54,6 +55,8 @@ struct mc_ctx {
   std::vector<int64_t> prob_begin;       // [n_probs+1]
   float* d_prob = nullptr;               // [n_probs * PROB_STRIDE]
   float* d_zc = nullptr;                 // [D * n]
+  double* d_alpha = nullptr;             // [D * n] fp64 design table
+  double* d_ctheta = nullptr;            // [n_probs * n * 2] (c_i theta_i, row scale bsc_i)
   int32_t* d_pod = nullptr;              // [D]
   int64_t* d_prob_begin = nullptr;       // [n_probs+1]
   int block_threads = 256;
@@ -76,6 +79,7 @@ mc_status launch_draw_dump(mc_ctx* c, const int64_t* design, const uint64_t* sam
                            cudaStream_t st);
 int draw_dump_stride(int n, int est);
 int words_per_draw(int n, int est);
+mc_status launch_zc(mc_ctx* c, cudaStream_t st);
 mc_status launch_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, cudaStream_t st);
 mc_status alpha_grid_solve(const mc_problem* probs, int32_t n_probs, int32_t m, int device,
                            std::vector<double>& alpha, std::vector<uint8_t>& valid);

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <math_constants.h>
 #include <cstdint>
 
 #include "mc_device.cuh"
@@ -26,15 +27,17 @@ __device__ __forceinline__ void load_problem(const float* __restrict__ rec, Prob
   for (int k = 0; k < N - 1; ++k) {
     pr.rho[k] = __ldg(rec + OFF_RHO + k);
     pr.sd[k] = __ldg(rec + OFF_SD + k);
-    pr.isd[k] = __ldg(rec + OFF_ISD + k);
+    pr.ris[k] = __ldg(rec + OFF_RIS + k);
   }
 }
 
 // fixed-point accumulation of one draw: q(x) = round-half-even(2^23 x) for x in [0,1] is the
-// mantissa of the fp32 sum x + 1 (one FADD / FFMA + one IADD3).
+// mantissa of the fp32 sum x + 1 (one FADD / FFMA + one IADD3).  IND: u in {0, 1}, u^2 = u, so only
+// the first sum is accumulated (the second is copied at the end).
+template <int EST>
 __device__ __forceinline__ void accumulate(float u, uint32_t& a1, uint32_t& a2) {
   a1 += __float_as_uint(u + 1.0f) - 0x3F800000u;
-  a2 += __float_as_uint(fmaf(u, u, 1.0f)) - 0x3F800000u;
+  if constexpr (EST == 0) a2 += __float_as_uint(fmaf(u, u, 1.0f)) - 0x3F800000u;
 }
 
 template <int N, int EST, bool MASKED>
@@ -45,6 +48,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
   constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
   static_assert(SAMPLES_PER_THREAD % G::L == 0, "L must divide the per-thread run");
   uint64_t q = s_begin * (uint64_t)G::U / 4;   // first Philox block of this thread's run
+  const uint32_t one = one_bits_reg();
 #pragma unroll 1
   for (int st = 0; st < STEPS; ++st) {
     const uint64_t s0 = s_begin + (uint64_t)st * G::L;
@@ -55,14 +59,15 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
     q += G::BLOCKS;
 #pragma unroll
     for (int l = 0; l < G::L; ++l) {
-      float u = draw_utility<N, EST, false>(&w[l * G::U], zc, pr);
+      float u = draw_utility<N, EST, false>(&w[l * G::U], one, zc, pr);
       if (MASKED) {
         const uint64_t s = s0 + l;
         u = (s >= B && s < E) ? u : 0.0f;
       }
-      accumulate(u, a1, a2);
+      accumulate<EST>(u, a1, a2);
     }
   }
+  if constexpr (EST == 1) a2 = a1;
 }
 
 template <int N, int EST>
@@ -171,6 +176,29 @@ int words_per_draw(int n, int est) {
 int draw_dump_stride(int n, int est) { return (est == 0 ? n : 2 * n) + n + 1; }
 
 // ---------------------------------------------------------------------------------------------
+// Design thresholds (row a1): zc_i = Z_{1-alpha_i} - c_i theta_i in fp64 -> fp32; alpha = 0 -> +inf.
+__global__ void k_zc(const double* __restrict__ alpha, const int32_t* __restrict__ pod, const double* __restrict__ ctheta,
+                     int n, int64_t D, float* __restrict__ zc) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= D * n) return;
+  const int64_t d = t / n;
+  const int i = (int)(t % n);
+  const double a = alpha[t];
+  const double z = a <= 0.0 ? CUDART_INF : -normcdfinv(a);   // Z_{1-a} = -Phi^{-1}(a)
+  const double* ct = ctheta + ((int64_t)pod[d] * n + i) * 2;  // (c_i theta_i, row scale)
+  zc[t] = (float)((z - ct[0]) * ct[1]);
+}
+
+mc_status launch_zc(mc_ctx* c, cudaStream_t st) {
+  const int64_t T = c->D * c->n;
+  if (T == 0) return MC_OK;
+  k_zc<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(c->d_alpha, c->d_pod, c->d_ctheta, c->n, c->D, c->d_zc);
+  c->launches += 1;
+  MC_CUDA(cudaGetLastError());
+  return MC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
 // K2: finalize (row a8), fp64.
 __global__ void k_finalize(const long long* __restrict__ sums, int64_t D, double N, double* __restrict__ mean,
                            double* __restrict__ var) {
@@ -188,6 +216,7 @@ mc_status launch_finalize(mc_ctx* c, const int64_t* sums, uint64_t N, double* me
   const int threads = 256;
   const int64_t blocks = (c->D + threads - 1) / threads;
   k_finalize<<<(unsigned)blocks, threads, 0, st>>>(reinterpret_cast<const long long*>(sums), c->D, (double)N, mean, var);
+  c->launches += 1;
   MC_CUDA(cudaGetLastError());
   return MC_OK;
 }
@@ -224,7 +253,9 @@ __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restr
   uint32_t w[G::U];
   const uint64_t base = sample[i] * (uint64_t)G::U;
   for (int k = 0; k < G::U; ++k) w[k] = philox_word(seed, (uint32_t)d, base + k);
-  draw_utility<N, EST, true>(w, zc, pr, out + i * G::DUMP);
+  float bsc[N];
+  for (int k = 0; k < N; ++k) bsc[k] = prob[(int64_t)pod[d] * PROB_STRIDE + OFF_BSC + k];
+  draw_utility<N, EST, true>(w, 0x3F800000u, zc, pr, out + i * G::DUMP, bsc);
 }
 
 template <int N, int EST>
@@ -291,6 +322,7 @@ __global__ void k_segmented_argmax(const double* __restrict__ values, const int6
 mc_status launch_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, cudaStream_t st) {
   if (c->n_probs == 0) return MC_OK;
   k_segmented_argmax<<<c->n_probs, 256, 0, st>>>(values, c->d_prob_begin, idx, val);
+  c->launches += 1;
   MC_CUDA(cudaGetLastError());
   return MC_OK;
 }

@@ -408,6 +408,7 @@ mc_status smooth_apply(mc_ctx* c, const double* values, double lambda, double* o
   k_et_y<<<dim3((unsigned)((kmax + 7) / 8), np), 256, 0, st>>>(pd, y, cc);
   k_gcv<<<np, 256, 0, st>>>(pd, lambda, cc, lam_tmp);
   k_e_c<<<dim3((unsigned)((Nmax + 127) / 128), np), 128, 0, st>>>(pd, y, cc, out);
+  c->launches += 4;
   MC_CUDA(cudaGetLastError());
   if (lam_used) {
     // scatter per-plan lambdas to their problem slots

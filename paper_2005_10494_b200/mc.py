@@ -61,6 +61,7 @@ def lib() -> ctypes.CDLL:
         L.mc_candidates.restype = i32
         L.mc_design_init.argtypes = [P(vp), P(mc_problem), i32, P(d), P(i32), i64, u64, i32, i32]
         L.mc_design_init.restype = i32
+        L.mc_design_upload.argtypes = [vp, P(d), vp]; L.mc_design_upload.restype = i32
         L.mc_set_launch.argtypes = [vp, i32, i32]; L.mc_set_launch.restype = i32
         L.mc_destroy.argtypes = [vp]; L.mc_destroy.restype = None
         L.mc_evaluate_grid.argtypes = [vp, i64, i64, u64, u64, vp, vp]; L.mc_evaluate_grid.restype = i32
@@ -80,7 +81,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_fwer", "mc_candidates",
-            "mc_design_init", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
+            "mc_design_init", "mc_design_upload", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
             "mc_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
 
@@ -235,6 +236,16 @@ class Design:
     @property
     def launches(self) -> int:
         return int(lib().mc_kernel_launches(self._ctx))
+
+    def upload(self, alpha_host, stream=None):
+        """Replace the design table from host memory (H2D + device thresholds); alpha_host may be a
+        pinned torch CPU tensor (async copy) or a numpy array."""
+        if hasattr(alpha_host, "data_ptr"):
+            ptr = ctypes.cast(alpha_host.data_ptr(), ctypes.POINTER(ctypes.c_double))
+        else:
+            alpha_host = np.ascontiguousarray(alpha_host, dtype=np.float64)
+            ptr = _dp(alpha_host)
+        _check(lib().mc_design_upload(self._ctx, ptr, _stream(stream)))
 
     def set_launch(self, block_threads: int = 0, grid_blocks: int = 0):
         _check(lib().mc_set_launch(self._ctx, block_threads, grid_blocks))
