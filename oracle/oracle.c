@@ -169,7 +169,7 @@ void or_null_corr(int n, const double *r, double *S)
  * Returns u in [0,1]: the success probability (COND) or indicator (IND).    */
 int or_words_per_draw(int n, int p, int est)
 {
-    if (est == 0) return 2 * ((p + 1) / 2) + (n - 1);
+    if (est == 0) return 2 * ((p + 1) / 2) + n / 2;
     return 2 * ((p + n + 1) / 2);
 }
 
@@ -217,20 +217,39 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
         }
         return reject ? 1.0 : 0.0;
     }
-    /* COND: Genz separation of variables in natural order.  With Y iid N(0,1),
-     * X = L0 Y; e_i = P(X_i <= b_i | y_1..y_{i-1}) = Phi((b_i - sum_{j<i} L0_ij y_j)/L0_ii),
-     * y_i = Phi^{-1}(v_i e_i).  prod_i e_i is an unbiased estimate of Phi_Sigma0(b).   */
+    /* COND: Genz separation of variables (SOV) for Phi_Sigma0(b) in the variable order
+     * pi = (populations 2, 4, 6, ..., then 1, 3, 5, ...).  With the permuted
+     * correlation S' = Sigma0[pi][pi] = L' L'^T, Y iid N(0,1), X_pi = L' Y:
+     *   e_a = P(X_pi(a) <= b_pi(a) | y_1..y_{a-1}) = Phi((b_pi(a) - sum_{j<a} L'_aj y_j) / L'_aa),
+     *   y_a = Phi^{-1}(v_a e_a),  and prod_a e_a is an unbiased estimate of Phi_Sigma0(b).
+     * Only the first n/2 (even-population) stages draw a uniform v_a: A.1 makes X a Markov chain,
+     * so every odd population is independent of the other odd ones given the even ones, i.e.
+     * L'_aj = 0 for j >= n/2 (checked below) and those y_j are never used.               */
     const int vbase = 2 * ((p + 1) / 2);
+    const int neven = n / 2;
+    int ord[OR_MAXN], k = 0;
+    for (int i = 1; i < n; i += 2) ord[k++] = i;     /* 0-based index of population 2, 4, ... */
+    for (int i = 0; i < n; i += 2) ord[k++] = i;     /* populations 1, 3, ... */
+    double Sp[OR_MAXN * OR_MAXN], Lq[OR_MAXN * OR_MAXN];
+    for (int a = 0; a < n; ++a)
+        for (int c = 0; c < n; ++c) Sp[a * n + c] = S0[ord[a] * n + ord[c]];
+    if (or_cholesky(n, Sp, Lq) != 0) return NAN;
     double y[OR_MAXN], prod = 1.0;
-    for (int i = 0; i < n; ++i) {
+    for (int a = 0; a < n; ++a) {
         double m = 0.0;
-        for (int j = 0; j < i; ++j) m += L0[i * n + j] * y[j];
-        double e = or_Phi((b[i] - m) / L0[i * n + i]);
+        for (int j = 0; j < a; ++j) {
+            if (j >= neven) {
+                if (fabs(Lq[a * n + j]) > 1e-12) return NAN;   /* the Markov zero of A.1 */
+                continue;
+            }
+            m += Lq[a * n + j] * y[j];
+        }
+        double e = or_Phi((b[ord[a]] - m) / Lq[a * n + a]);
         prod *= e;
-        if (prod == 0.0) break;                       /* u = 1 exactly; later y are irrelevant */
-        if (i + 1 < n) {
-            double v = u_open(or_word(seed, design, w0 + vbase + i));
-            y[i] = or_Phi_inv(v * e);
+        if (prod == 0.0) break;                        /* u = 1 exactly; later stages are irrelevant */
+        if (a < neven) {
+            double v = u_open(or_word(seed, design, w0 + vbase + a));
+            y[a] = or_Phi_inv(v * e);
         }
     }
     return 1.0 - prod;

@@ -100,14 +100,67 @@ static mc_status validate_problem(const mc_problem& p, int idx) {
 
 constexpr double BM_K = 1.17741002251547469;   // sqrt(2 ln 2), see mc_device.cuh
 
+// COND stage coefficients of the SOV order (2, 4, ..., 1, 3, ...) for the Formula-1 Markov chain
+// (A.1): X_{j+1} = rho_j X_j + s_j W (0-based j).  Even populations (0-based p = 2k+1) form the chain
+// X_p | X_{p-2} ~ N(mu x, sd^2), mu = rho_{p-2} rho_{p-1}; odd ones (p = 2j) are Gaussian bridges
+// X_p | X_{p-1} = a, X_{p+1} = c ~ N(alpha a + beta c, gamma^2).  Returns the conditional sd of
+// population p's stage (its row scale is 1/sd) and the stage coefficients.
+struct SovCoef {
+  double sd[MC_MAX_N];                      // per population
+  double emu[MC_MAX_N], esd[MC_MAX_N];      // even stages
+  double oa[MC_MAX_N], ob[MC_MAX_N];        // odd stages: alpha, beta (unscaled)
+};
+
+static SovCoef sov_coef(const mc_problem& p) {
+  const int n = p.n;
+  double rho[MC_MAX_N] = {0}, s[MC_MAX_N] = {0};
+  for (int i = 0; i + 1 < n; ++i) {
+    rho[i] = std::sqrt(p.r[i + 1] / p.r[i]);
+    s[i] = std::sqrt(1.0 - p.r[i + 1] / p.r[i]);
+  }
+  SovCoef c{};
+  for (int k = 0; 2 * k + 1 < n; ++k) {
+    const int q = 2 * k + 1;
+    if (k == 0) { c.emu[k] = 0.0; c.esd[k] = 1.0; }
+    else {
+      const double mu = rho[q - 2] * rho[q - 1];
+      c.emu[k] = mu;
+      c.esd[k] = std::sqrt(1.0 - mu * mu);
+    }
+    c.sd[q] = c.esd[k];
+  }
+  for (int j = 0; 2 * j < n; ++j) {
+    const int q = 2 * j;
+    const bool L = q >= 1, R = q + 1 < n;
+    double a = 0.0, bb = 0.0, g = 1.0;
+    if (L && R) {
+      const double prec = 1.0 / (s[q - 1] * s[q - 1]) + rho[q] * rho[q] / (s[q] * s[q]);
+      const double g2 = 1.0 / prec;
+      a = rho[q - 1] / (s[q - 1] * s[q - 1]) * g2;
+      bb = rho[q] / (s[q] * s[q]) * g2;
+      g = std::sqrt(g2);
+    } else if (R) {             // q = 0: X_0 | X_1 = c ~ N(rho_0 c, s_0^2)
+      bb = rho[0];
+      g = s[0];
+    } else if (L) {             // last population, n odd: X_q | X_{q-1} = a ~ N(rho_{q-1} a, s_{q-1}^2)
+      a = rho[q - 1];
+      g = s[q - 1];
+    }
+    c.oa[j] = a;
+    c.ob[j] = bb;
+    c.sd[q] = g;
+  }
+  return c;
+}
+
 // Row scale of b folded into the record and the thresholds (mc_device.cuh ProbRegs).
 static double row_scale(const mc_problem& p, int est, int i) {
   if (est == MC_EST_IND) return 1.0 / BM_K;
-  return i == 0 ? 1.0 : 1.0 / std::sqrt(1.0 - p.r[i] / p.r[i - 1]);
+  return 1.0 / sov_coef(p).sd[i];
 }
 
-// Per-problem device record (fp32): M = diag(c) L_p packed with the folded scales, rho, s, rho/s,
-// row scales (Formula 1/3/10, A.1).
+// Per-problem device record (fp32): M = diag(c) L_p packed with the folded scales, the IND Markov
+// coefficients, the COND stage coefficients and the row scales (Formula 1/3/10, A.1).
 static void problem_record(const mc_problem& p, int est, float* rec) {
   const int n = p.n;
   double rho[MC_MAX_N] = {0}, sd[MC_MAX_N] = {0};
@@ -126,6 +179,7 @@ static void problem_record(const mc_problem& p, int est, float* rec) {
   for (int i = 0; i < n; ++i)
     for (int j = 0; j <= i; ++j)
       Lp[i][j] = p.has_prior_chol ? p.prior_chol[i * MC_MAX_N + j] : p.sigma[i] * L0[i][j];
+  const SovCoef sc = sov_coef(p);
   std::fill(rec, rec + PROB_STRIDE, 0.0f);
   for (int i = 0; i < n; ++i) {
     const double c = std::sqrt(p.r[i] * p.i3);
@@ -137,7 +191,15 @@ static void problem_record(const mc_problem& p, int est, float* rec) {
   for (int i = 0; i + 1 < n; ++i) {
     rec[OFF_RHO + i] = (float)rho[i];
     rec[OFF_SD + i] = (float)sd[i];
-    rec[OFF_RIS + i] = (float)(rho[i] / sd[i]);
+  }
+  for (int k = 0; 2 * k + 1 < n; ++k) {
+    rec[OFF_ER + k] = (float)(sc.emu[k] / sc.esd[k]);
+    rec[OFF_EMU + k] = (float)sc.emu[k];
+    rec[OFF_ESD + k] = (float)sc.esd[k];
+  }
+  for (int j = 0; 2 * j < n; ++j) {
+    rec[OFF_OA + j] = (float)(sc.oa[j] / sc.sd[2 * j]);
+    rec[OFF_OB + j] = (float)(sc.ob[j] / sc.sd[2 * j]);
   }
 }
 

@@ -19,7 +19,9 @@ struct Geo {
   static constexpr int P = N;
   static constexpr int NNORM = (EST == 0) ? P : P + N;          // normals per draw
   static constexpr int NPAIR = (NNORM + 1) / 2;                   // Box-Muller pairs
-  static constexpr int U = (EST == 0) ? 2 * ((P + 1) / 2) + (N - 1) : 2 * NPAIR;  // words per draw
+  static constexpr int U = (EST == 0) ? 2 * ((P + 1) / 2) + N / 2 : 2 * NPAIR;   // words per draw
+  static constexpr int NE = N / 2;           // COND: even populations (sampled), 0-based index 2k+1
+  static constexpr int NO = (N + 1) / 2;     // COND: odd populations (analytic), 0-based index 2j
   static constexpr int L = 4 / cgcd(U, 4);                        // draws per Philox-aligned step
   static constexpr int BLOCKS = U * L / 4;                        // Philox blocks per step
   static constexpr int NM = N * (N + 1) / 2;                      // packed lower-triangular M
@@ -29,6 +31,22 @@ struct Geo {
 // ---------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11).  Counter (q_lo, q_hi, design, 0), key (seed_lo, seed_hi).
 struct Key { uint32_t k0, k1; };
+// The ten round keys (k0 + r W0, k1 + r W1), r = 0..9, precomputed on the host and passed by value
+// as a kernel parameter: the rounds then read them straight from the constant bank (no key schedule
+// in the loop).
+struct RoundKeys { uint32_t k0[10], k1[10]; };
+
+__host__ __device__ inline RoundKeys round_keys(uint64_t seed) {
+  RoundKeys rk;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    rk.k0[r] = k0;
+    rk.k1[r] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return rk;
+}
 
 // 32x32 -> 64-bit product as ONE IMAD.WIDE.U32 (ptxas otherwise often splits it into IMAD.HI + IMAD).
 __device__ __forceinline__ void mulhilo(uint32_t a, uint32_t m, uint32_t& hi, uint32_t& lo) {
@@ -68,6 +86,21 @@ __device__ __forceinline__ void philox_block(uint64_t q, uint32_t lo1d, uint32_t
     k1 += 0xBB67AE85u;
     philox_round(c0, c1, c2, c3, k0, k1);
   }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// Same block with the precomputed round keys (the fused kernel's form).
+__device__ __forceinline__ void philox_block_rk(uint64_t q, uint32_t lo1d, uint32_t hi1d, const RoundKeys& rk,
+                                                uint32_t out[4]) {
+  const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32);
+  uint32_t hq, lq;
+  mulhilo(q0, 0xD2511F53u, hq, lq);
+  uint32_t c0 = hi1d ^ q1 ^ rk.k0[0];
+  uint32_t c1 = lo1d;
+  uint32_t c2 = hq ^ rk.k1[0];
+  uint32_t c3 = lq;
+#pragma unroll
+  for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
   out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
@@ -245,15 +278,22 @@ __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Per-problem parameters in registers (loaded once per tile; uniform across the block).  The device
-// record folds constant factors (mc_api.cu problem_record()):
-//   COND: row i of M and zc carry bs_i = (i == 0 ? 1 : 1/s_{i-1}), M also BM_K, so the kernel's
-//         b'_i = b_i bs_i and the SOV stage argument is a_i = b'_i - (rho_{i-1}/s_{i-1}) x_{i-1}.
-//   IND:  zc carries 1/BM_K and M is unscaled: b' = b / BM_K compared with X' = X / BM_K.
+// Per-problem parameters in registers (loaded once per tile; uniform across the block).
+//
+// COND evaluates the SOV in the order (populations 2, 4, ..., then 1, 3, ...): by the
+// Markov structure of A.1 the even populations form a chain X_{2k+2} | X_{2k} ~ N(mu x, sd^2) and each
+// odd population is conditionally independent of the rest given its even neighbours (a Gaussian
+// bridge).  The device record folds the conditional standard deviations into the rows of M and zc
+// (mc_api.cu problem_record()), so every stage argument is one or two FFMAs:
+//   even k:  a = b'_{2k+1} - er_k x_{k-1},  x_k = emu_k x_{k-1} + esd_k Phi^{-1}(v_k e_k)
+//   odd  j:  a = b'_{2j} - oa_j x_{j-1} - ob_j x_j
+// IND uses the natural Markov recursion (rho, s) with b' = b / BM_K.
 template <int N>
 struct ProbRegs {
+  static constexpr int NE = N / 2 > 0 ? N / 2 : 1, NO = (N + 1) / 2, NR = N > 1 ? N - 1 : 1;
   float M[N * (N + 1) / 2];   // packed lower triangular (row i: M[i(i+1)/2 + j])
-  float rho[N > 1 ? N - 1 : 1], sd[N > 1 ? N - 1 : 1], ris[N > 1 ? N - 1 : 1];   // rho, s, rho/s
+  float rho[NR], sd[NR];      // IND
+  float er[NE], emu[NE], esd[NE], oa[NO], ob[NO];   // COND
 };
 
 // One draw from its U words w[0..U): returns u in [0,1].  If DBG, writes the (unscaled) normals,
@@ -274,7 +314,7 @@ __device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, c
     for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
     b[i] = acc;
   }
-  float u;
+  float u = 0.0f;
   if constexpr (EST == 1) {
     // Formula 6/7: one null draw X = L0 W (Markov recursion), success iff some X_i > b_i.
     float x = nrm[G::P];
@@ -286,26 +326,27 @@ __device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, c
     }
     u = rej ? 1.0f : 0.0f;
   } else {
-    // COND: u = 1 - prod e_i accumulated as u <- u + (1 - u) q_i (q_i = 1 - e_i, no cancellation).
+    // COND: u = 1 - prod e accumulated as u <- u + (1 - u) q (q = 1 - e: no cancellation).
     constexpr int VB = 2 * ((G::P + 1) / 2);
+    float x[G::NE > 0 ? G::NE : 1];
     float q, e;
-    normal_tail(b[0], q, e);     // q = Phi(-b1) = P(X1 > b1), e = Phi(b1)
-    u = q;
-    float x = 0.0f;
-    if constexpr (N > 1) {
-      const float v = word_to_f12(w[VB], one) - 0.99999994039535522f;  // (k + 1/2) 2^-23
-      const float vc = 1.0f - v;                                       // exact
-      x = normal_quantile_fast(v * e, fmaf(v, q, vc));
+#pragma unroll
+    for (int k = 0; k < G::NE; ++k) {
+      const float a = k == 0 ? b[1] : fmaf(-pr.er[k], x[k - 1], b[2 * k + 1]);
+      normal_tail(a, q, e);
+      u = k == 0 ? q : fmaf(1.0f - u, q, u);
+      const float v = word_to_f12(w[VB + k], one) - 0.99999994039535522f;   // (k + 1/2) 2^-23
+      const float vc = 1.0f - v;                                            // exact
+      const float y = normal_quantile_fast(v * e, fmaf(v, q, vc));
+      x[k] = k == 0 ? y : fmaf(pr.esd[k], y, pr.emu[k] * x[k - 1]);
     }
 #pragma unroll
-    for (int i = 1; i < N; ++i) {
-      normal_tail(fmaf(-pr.ris[i - 1], x, b[i]), q, e);
-      u = fmaf(1.0f - u, q, u);
-      if (i + 1 < N) {
-        const float v = word_to_f12(w[VB + i], one) - 0.99999994039535522f;
-        const float vc = 1.0f - v;
-        x = fmaf(pr.sd[i - 1], normal_quantile_fast(v * e, fmaf(v, q, vc)), pr.rho[i - 1] * x);
-      }
+    for (int j = 0; j < G::NO; ++j) {
+      float a = b[2 * j];
+      if (2 * j >= 1) a = fmaf(-pr.oa[j], x[j - 1], a);
+      if (2 * j + 1 < N) a = fmaf(-pr.ob[j], x[j], a);
+      normal_tail(a, q, e);
+      u = (G::NE == 0 && j == 0) ? q : fmaf(1.0f - u, q, u);
     }
   }
   if constexpr (DBG) {

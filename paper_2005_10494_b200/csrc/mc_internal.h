@@ -12,12 +12,17 @@ namespace mci {
 
 constexpr int PROB_STRIDE = 112;         // floats per device problem record
 constexpr int OFF_M = 0;                 // packed M = diag(c) L_p with the folded row scales (55 floats for n = 10)
-constexpr int OFF_RHO = 56;              // rho_i = sqrt(r_{i+1}/r_i)
-constexpr int OFF_SD = 66;               // s_i = sqrt(1 - rho_i^2)
-constexpr int OFF_RIS = 76;              // rho_i / s_i
-constexpr int OFF_BSC = 86;              // row scale of b' = b * bsc (dump only)
-constexpr int SAMPLES_PER_THREAD = 64;   // per-thread sample run inside a tile
+constexpr int OFF_RHO = 56;              // IND: rho_i = sqrt(r_{i+1}/r_i)
+constexpr int OFF_SD = 66;               // IND: s_i = sqrt(1 - rho_i^2)
+constexpr int OFF_ER = 76;               // COND even stage k: mu_k / sd_k
+constexpr int OFF_EMU = 81;              // COND even stage k: mu_k (coefficient of x_{k-1})
+constexpr int OFF_ESD = 86;              // COND even stage k: conditional sd_k
+constexpr int OFF_OA = 91;               // COND odd stage j: left-neighbour coefficient / gamma_j
+constexpr int OFF_OB = 96;               // COND odd stage j: right-neighbour coefficient / gamma_j
+constexpr int OFF_BSC = 101;             // row scale of b' = b * bsc (dump only)
+constexpr int SAMPLES_PER_THREAD = 128;  // per-thread sample run inside a warp tile (< 512: u32 sums)
 constexpr int MAX_BLOCK = 256;           // fused kernel __launch_bounds__
+constexpr int MIN_BLOCKS = 4;            // ... and min resident blocks per SM (register cap 64)
 
 void set_error(const std::string& msg);
 mc_status cuda_fail(cudaError_t e, const char* where);

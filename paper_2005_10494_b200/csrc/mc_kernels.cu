@@ -1,11 +1,11 @@
 // mc_kernels.cu — K1 fused Monte-Carlo kernel, K2 finalize, K3 Philox dump, draw dump, K6 argmax.
 //
-// K1 (rows a2-a6 of DESIGN.md §1): persistent grid over tiles (design, 64*blockDim samples).
-// Each thread owns 64 consecutive samples of one design, generates their Philox words in
+// K1 (rows a2-a6 of DESIGN.md §1): persistent grid over warp tiles (design, 32 x 128 samples).
+// Each thread owns 128 consecutive samples of one design, generates their Philox words in
 // registers (U words per draw, L draws per aligned step), evaluates u, and accumulates the exact
-// 2^-23 fixed-point sums in 32-bit registers; a 64-bit warp shuffle + shared-memory block reduction
-// then issues one 64-bit atomicAdd pair per (block, design tile).  Integer sums make the result
-// independent of the launch shape.
+// 2^-23 fixed-point sums in 32-bit registers; a 64-bit warp shuffle reduction then issues one 64-bit
+// atomicAdd pair per warp tile (no block barrier).  Integer sums make the result independent of the
+// launch shape.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -27,7 +27,17 @@ __device__ __forceinline__ void load_problem(const float* __restrict__ rec, Prob
   for (int k = 0; k < N - 1; ++k) {
     pr.rho[k] = __ldg(rec + OFF_RHO + k);
     pr.sd[k] = __ldg(rec + OFF_SD + k);
-    pr.ris[k] = __ldg(rec + OFF_RIS + k);
+  }
+#pragma unroll
+  for (int k = 0; k < N / 2; ++k) {
+    pr.er[k] = __ldg(rec + OFF_ER + k);
+    pr.emu[k] = __ldg(rec + OFF_EMU + k);
+    pr.esd[k] = __ldg(rec + OFF_ESD + k);
+  }
+#pragma unroll
+  for (int k = 0; k < (N + 1) / 2; ++k) {
+    pr.oa[k] = __ldg(rec + OFF_OA + k);
+    pr.ob[k] = __ldg(rec + OFF_OB + k);
   }
 }
 
@@ -42,7 +52,7 @@ __device__ __forceinline__ void accumulate(float u, uint32_t& a1, uint32_t& a2) 
 
 template <int N, int EST, bool MASKED>
 __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64_t E, uint32_t lo1d, uint32_t hi1d,
-                                            Key key, const float* zc, const ProbRegs<N>& pr, uint32_t& a1,
+                                            const RoundKeys& rk, const float* zc, const ProbRegs<N>& pr, uint32_t& a1,
                                             uint32_t& a2) {
   using G = Geo<N, EST>;
   constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
@@ -55,7 +65,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
     if (MASKED && s0 >= E) break;
     uint32_t w[G::BLOCKS * 4];
 #pragma unroll
-    for (int b = 0; b < G::BLOCKS; ++b) philox_block(q + b, lo1d, hi1d, key, &w[4 * b]);
+    for (int b = 0; b < G::BLOCKS; ++b) philox_block_rk(q + b, lo1d, hi1d, rk, &w[4 * b]);
     q += G::BLOCKS;
 #pragma unroll
     for (int l = 0; l < G::L; ++l) {
@@ -70,17 +80,21 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
   if constexpr (EST == 1) a2 = a1;
 }
 
+// Work unit = one WARP tile: (design, 32 x SAMPLES_PER_THREAD consecutive samples).  Warps are
+// independent (no block barrier): each reduces its tile with 64-bit shuffles and lane 0 issues one
+// 64-bit atomicAdd pair.  Warp tiles are strided over the persistent grid's warps.
+constexpr int min_blocks(int n) { return n <= 3 ? MIN_BLOCKS : (n <= 5 ? 2 : 1); }
+
 template <int N, int EST>
-__global__ void __launch_bounds__(MAX_BLOCK) mc_fused_kernel(const float* __restrict__ prob, const float* __restrict__ zc_all,
-                                                             const int32_t* __restrict__ pod, int64_t d0,
-                                                             uint64_t B, uint64_t E, uint64_t Balign,
-                                                             int64_t tiles_per_design, int64_t total_tiles,
-                                                             uint64_t seed, unsigned long long* __restrict__ sums) {
-  __shared__ unsigned long long red[2][MAX_BLOCK / 32];
-  const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const uint64_t tile_samples = (uint64_t)blockDim.x * SAMPLES_PER_THREAD;
-  for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+__global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N)) mc_fused_kernel(
+    const float* __restrict__ prob, const float* __restrict__ zc_all, const int32_t* __restrict__ pod, int64_t d0,
+    uint64_t B, uint64_t E, uint64_t Balign, int64_t tiles_per_design, int64_t total_tiles, const RoundKeys rk,
+    unsigned long long* __restrict__ sums) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  constexpr uint64_t tile_samples = 32ull * SAMPLES_PER_THREAD;
+  for (int64_t tile = gw; tile < total_tiles; tile += nw) {
     const int64_t d = d0 + tile / tiles_per_design;
     const int64_t chunk = tile % tiles_per_design;
     ProbRegs<N> pr;
@@ -90,27 +104,22 @@ __global__ void __launch_bounds__(MAX_BLOCK) mc_fused_kernel(const float* __rest
     for (int i = 0; i < N; ++i) zc[i] = __ldg(zc_all + d * N + i);
     const uint32_t dd = (uint32_t)d;
     const uint32_t lo1d = 0xCD9E8D57u * dd, hi1d = __umulhi(0xCD9E8D57u, dd);
-    const uint64_t s_begin = Balign + (uint64_t)chunk * tile_samples + (uint64_t)threadIdx.x * SAMPLES_PER_THREAD;
+    const uint64_t s_begin = Balign + (uint64_t)chunk * tile_samples + (uint64_t)lane * SAMPLES_PER_THREAD;
     uint32_t a1 = 0, a2 = 0;
     if (s_begin >= B && s_begin + SAMPLES_PER_THREAD <= E)
-      run_samples<N, EST, false>(s_begin, B, E, lo1d, hi1d, key, zc, pr, a1, a2);
+      run_samples<N, EST, false>(s_begin, B, E, lo1d, hi1d, rk, zc, pr, a1, a2);
     else if (s_begin < E)
-      run_samples<N, EST, true>(s_begin, B, E, lo1d, hi1d, key, zc, pr, a1, a2);
+      run_samples<N, EST, true>(s_begin, B, E, lo1d, hi1d, rk, zc, pr, a1, a2);
     unsigned long long v1 = a1, v2 = a2;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       v1 += __shfl_xor_sync(0xffffffffu, v1, o);
       v2 += __shfl_xor_sync(0xffffffffu, v2, o);
     }
-    if (lane == 0) { red[0][warp] = v1; red[1][warp] = v2; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t1 = 0, t2 = 0;
-      for (int k = 0; k < nwarps; ++k) { t1 += red[0][k]; t2 += red[1][k]; }
-      atomicAdd(sums + 2 * d, t1);
-      atomicAdd(sums + 2 * d + 1, t2);
+    if (lane == 0) {
+      atomicAdd(sums + 2 * d, v1);
+      atomicAdd(sums + 2 * d + 1, v2);
     }
-    __syncthreads();
   }
 }
 
@@ -119,7 +128,7 @@ static cudaError_t launch_fused_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_
                                   int64_t* sums) {
   using G = Geo<N, EST>;
   const int threads = c->block_threads;
-  const uint64_t tile = (uint64_t)threads * SAMPLES_PER_THREAD;
+  const uint64_t tile = 32ull * SAMPLES_PER_THREAD;   // one warp tile
   const uint64_t Balign = B - (B % G::L);
   const int64_t tpd = (int64_t)((E - Balign + tile - 1) / tile);
   const int64_t total = tpd * dcount;
@@ -131,10 +140,11 @@ static cudaError_t launch_fused_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mc_fused_kernel<N, EST>, threads, 0);
     grid = nsm * (per > 0 ? per : 1);
   }
-  if ((int64_t)grid > total) grid = (int)total;
+  const int64_t warps_needed = total, wpb = threads / 32;
+  if ((int64_t)grid * wpb > warps_needed) grid = (int)((warps_needed + wpb - 1) / wpb);
   if (grid <= 0) return cudaSuccess;
   mc_fused_kernel<N, EST><<<grid, threads, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, d0, B, E, Balign, tpd, total,
-                                                    c->seed, reinterpret_cast<unsigned long long*>(sums));
+                                                    round_keys(c->seed), reinterpret_cast<unsigned long long*>(sums));
   c->launches += 1;
   return cudaGetLastError();
 }
@@ -171,7 +181,7 @@ mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64
 
 int words_per_draw(int n, int est) {
   // Geo<N,EST>::U without instantiating every N
-  return est == 0 ? 2 * ((n + 1) / 2) + (n - 1) : 2 * ((2 * n + 1) / 2);
+  return est == 0 ? 2 * ((n + 1) / 2) + n / 2 : 2 * ((2 * n + 1) / 2);
 }
 int draw_dump_stride(int n, int est) { return (est == 0 ? n : 2 * n) + n + 1; }
 

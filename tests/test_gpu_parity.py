@@ -250,3 +250,45 @@ def test_general_prior_and_n5(O, mc, torch):
     op = O.Problem(r=np.array(r), i3=211.0, alpha0=0.025, theta=theta, prior_cov=cov)
     ref = O.finalize(O.design_sums(op, alpha[0], 0, SEED, 0, 0, N), N)[0][0]
     assert abs(got - ref) <= REL * ref
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 10])
+@pytest.mark.parametrize("est", [0, 1])
+def test_dimension_sweep_parity(O, mc, torch, n, est):
+    """C5-shaped problems (r_i = (n-i+1)/n, scenario (c)) for every template width: the SOV stage
+    program (even chain + odd bridges) and the IND recursion against the oracle's generic Cholesky."""
+    spec = W.c5_problem(n)
+    op = oracle_problem(O, spec)
+    alphas = []
+    for a1 in (0.004, 0.012):
+        if n == 1:
+            alphas.append([0.025])
+            break
+        rest = O.solve_alpha_n(spec.r, spec.alpha0, [a1] + [0.0] * (n - 2), 1e-12)
+        # equal split of the remaining budget over populations 2..n is solved on alpha_n only:
+        mid = [a1] + [0.002] * (n - 2)
+        an = O.solve_alpha_n(spec.r, spec.alpha0, mid, 1e-12)
+        alphas.append(mid + [an] if an is not None else [a1] + [0.0] * (n - 2) + [rest])
+    alpha = np.array(alphas)
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(len(alpha), dtype=np.int32), seed=SEED, estimator=est)
+    N = 30_000
+    sums = dsg.new_sums()
+    dsg.evaluate(sums, 0, N)
+    got = dsg.finalize(sums, N)[0].cpu().numpy()
+    for d in range(len(alpha)):
+        ref_s = _oracle_sums(O, op, alpha[d], est, d, 0, N)
+        ref = O.finalize(ref_s, N)[0][0]
+        if est == 0:
+            assert abs(got[d] - ref) <= REL * ref, (n, d, got[d], ref)
+        else:
+            assert abs(int(sums[d, 0].item()) - int(ref_s[0])) // 2**23 <= 2
+    # per-draw records for the same designs
+    D = torch.tensor([0, len(alpha) - 1] * 16).cuda()
+    S = torch.arange(32).cuda() * 7919
+    rec = dsg.draw_dump(D, S).cpu().numpy()
+    for i in range(32):
+        o = O.draw(op, alpha[int(D[i])], est, SEED, int(D[i]), int(S[i]))
+        if est == 0:
+            assert abs(rec[i, -1] - o["u"]) <= 5e-5
+        else:
+            assert rec[i, -1] == o["u"] or np.min(np.abs(o["xnull"] - o["b"])) < 1e-4

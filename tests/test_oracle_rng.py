@@ -38,12 +38,12 @@ def test_word_stream_layout(O):
 
 
 def test_words_per_draw(O):
-    # COND: 2*ceil(p/2) Box-Muller words + (n-1) SOV uniforms; IND: 2*ceil((p+n)/2)
-    assert O.words_per_draw(3, 3, 0) == 6
+    # COND: 2*ceil(p/2) Box-Muller words + floor(n/2) SOV uniforms (even populations); IND: 2*ceil((p+n)/2)
+    assert O.words_per_draw(3, 3, 0) == 5
     assert O.words_per_draw(3, 3, 1) == 6
     assert O.words_per_draw(1, 1, 0) == 2
     assert O.words_per_draw(2, 2, 0) == 3
-    assert O.words_per_draw(10, 10, 0) == 19
+    assert O.words_per_draw(10, 10, 0) == 15
     assert O.words_per_draw(10, 10, 1) == 20
 
 

@@ -1,23 +1,40 @@
 """Count the issue slots per draw of the fused kernel's steady-state loop from its sm_100a SASS.
 
-The unmasked per-thread loop of mc_fused_kernel<N, EST> is the block ending in the backward branch
-with the largest body.  Inside it, every inverse-normal-CDF call has a three-way branch (central,
-tail, deep tail); the common path takes the central polynomial, so the tail blocks are subtracted.
-Prints the opcode histogram and issue slots per draw (used as bench.py ISSUE_PER_DRAW).
+The steady-state loop of mc_fused_kernel<N, EST> (unmasked per-thread run) is walked from the
+target of its backward branch along the COMMON path:
+  * `BRA.DIV` (divergence fallback of a warp vote) is not taken;
+  * `@!P BRA` right after `VOTE.ANY P` (the warp-uniform rare inverse-CDF tail) is taken, i.e. the
+    tail polynomials are skipped;
+  * unconditional forward `BRA` is followed; other conditional forward branches fall through.
+Issue slots per draw = path length / draws per iteration.  Used by bench.py for the ALU roofline.
 
     python tools/sass_count.py [N] [EST]
 """
 import collections
+import os
 import re
 import subprocess
 import sys
 
-LIB = "paper_2005_10494_b200/libmc_design.so"
+LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2005_10494_b200", "libmc_design.so")
+def draws_per_iter(n: int, est: int) -> int:
+    """L = 4 / gcd(U, 4) draws per Philox-aligned step (mc_device.cuh Geo)."""
+    import math
+    U = 2 * ((n + 1) // 2) + n // 2 if est == 0 else 2 * n
+    return 4 // math.gcd(U, 4)
 
 
-def sass(n: int, est: int):
-    sym = f"_ZN3mci15mc_fused_kernelILi{n}ELi{est}EEEvPKfS2_PKilmmmllmPy"
-    out = subprocess.run(["cuobjdump", "-sass", "-fun", sym, LIB], capture_output=True, text=True).stdout
+def sass(n: int, est: int, lib: str = None):
+    out = subprocess.run(["cuobjdump", "-sass", lib or LIB], capture_output=True, text=True).stdout
+    # select the function body of mc_fused_kernel<n, est>
+    tag = f"_ZN3mci15mc_fused_kernelILi{n}ELi{est}EEEv"
+    lines, on = [], False
+    for line in out.splitlines():
+        if "Function :" in line:
+            on = tag in line
+        elif on:
+            lines.append(line)
+    out = "\n".join(lines)
     ins = []
     for line in out.splitlines():
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
@@ -26,63 +43,71 @@ def sass(n: int, est: int):
     return ins
 
 
-def loop_body(ins):
+def _target(text):
+    m = re.search(r"\bBRA(?:\.\w+)?\s+(?:U?P\w+,\s*)?(?:UR\w+,\s*)?0x([0-9a-f]+)", text)
+    return int(m.group(1), 16) if m else None
+
+
+def walk(ins, start, end):
+    """Common path from address `start` until the back edge at `end`."""
+    idx = {a: i for i, (a, _) in enumerate(ins)}
+    i = idx[start]
+    path = []
+    prev = ""
+    for _ in range(20000):
+        a, t = ins[i]
+        path.append((a, t))
+        if a == end:
+            break
+        tgt = _target(t)
+        if tgt is not None and "BRA" in t:
+            if "BRA.DIV" in t:
+                i += 1
+            elif t.startswith("@!P") and prev.startswith("VOTE.ANY P"):
+                i = idx[tgt]
+            elif t.startswith("@P") and ("FSETP.GEU" in prev and (", 5," in prev or ", 16," in prev)):
+                i += 1          # w >= 5 / w >= 16: the inverse-CDF tails, not taken on the common path
+            elif not t.startswith("@") and tgt > a:
+                i = idx[tgt]
+            else:
+                i += 1
+        else:
+            i += 1
+        if i >= len(ins):
+            break
+        prev = t
+    return path
+
+
+def steady_loop(ins):
+    """The innermost sample loop: the shortest back-edge cycle that evaluates draws (has MUFU) and
+    contains no block barrier (which marks the outer tile loop); the masked variant is longer."""
     best = None
-    for addr, text in ins:
-        m = re.search(r"\bBRA\s+(?:\w+,\s*)?0x([0-9a-f]+)", text)
-        if m:
-            tgt = int(m.group(1), 16)
-            if tgt < addr and (best is None or addr - tgt > best[1] - best[0]):
-                best = (tgt, addr)
-    lo, hi = best
-    return [(a, t) for a, t in ins if lo <= a <= hi]
-
-
-def common_path(body):
-    """Drop the tail branches of the quantile: from each `FMNMX Rx, Ry, 88` (tail entry) up to the
-    join target of the preceding central block's BRA."""
-    keep = []
-    skip_until = None
-    for i, (a, t) in enumerate(body):
-        if skip_until is not None:
-            if a < skip_until:
+    for a, t in ins:
+        tgt = _target(t)
+        if tgt is not None and tgt < a and "BRA" in t:
+            p = walk(ins, tgt, a)
+            if p[-1][0] != a or any(x.startswith("BAR") for _, x in p):
                 continue
-            skip_until = None
-        if t.startswith("FMNMX") and ", 88" in t:
-            # the central block ends with `BRA join` just before this instruction
-            prev = body[i - 1][1]
-            m = re.search(r"BRA\s+0x([0-9a-f]+)", prev)
-            skip_until = int(m.group(1), 16)
-            keep.pop()   # the central block's BRA is not executed as a taken jump on the fall-through path
-            keep.append((body[i - 1][0], "BRA(central->join)"))
-            continue
-        keep.append((a, t))
-    return keep
-
-
-DRAWS_PER_ITER = {0: {1: 2, 2: 4, 3: 2}, 1: {1: 2, 2: 1, 3: 2}}
+            if not any(x.startswith("MUFU") for _, x in p):
+                continue
+            if best is None or len(p) < len(best):
+                best = p
+    return best
 
 
 def issue_per_draw(n: int = 3, est: int = 0, lib: str = None) -> float:
-    """Common-path issue slots per draw of mc_fused_kernel<n, est> in the built library."""
-    global LIB
-    if lib:
-        LIB = lib
-    path = common_path(loop_body(sass(n, est)))
-    return len(path) / DRAWS_PER_ITER[est][n]
+    return len(steady_loop(sass(n, est, lib))) / draws_per_iter(n, est)
 
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     est = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-    ins = sass(n, est)
-    body = loop_body(ins)
-    path = common_path(body)
-    L = DRAWS_PER_ITER.get(est, {}).get(n, 2)
-    op = collections.Counter(t.split()[0].lstrip("@!P0123456789T ").split(".")[0] if not t.startswith("@")
-                             else t.split()[1].split(".")[0] for _, t in path)
-    print(f"mc_fused_kernel<{n},{est}>: loop body {len(body)} instr, common path {len(path)} instr, "
-          f"{L} draws/iteration -> {len(path) / L:.1f} issue slots/draw")
+    path = steady_loop(sass(n, est))
+    L = draws_per_iter(n, est)
+    op = collections.Counter((t.split()[1] if t.startswith("@") else t.split()[0]).split(".")[0] for _, t in path)
+    print(f"mc_fused_kernel<{n},{est}>: common path {len(path)} instr, {L} draws/iteration -> "
+          f"{len(path) / L:.1f} issue slots/draw")
     for k, v in op.most_common():
         print(f"  {k:12s} {v:4d}  ({v / L:.1f}/draw)")
 
