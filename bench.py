@@ -33,7 +33,7 @@ from paper_2005_10494_b200 import workloads as W  # noqa: E402
 # Per-draw issue slots of the fused kernel's steady-state loop (n = 3), counted from the sm_100a SASS
 # of the library being timed by tools/sass_count.py: the ALU/issue roofline's work per
 # draw.  The fallback constants are that tool's output for the committed kernel.
-ISSUE_PER_DRAW_FALLBACK = {"cond": 171.0, "ind": 112.5}
+ISSUE_PER_DRAW_FALLBACK = {"cond": 181.75, "ind": 112.5}
 
 
 def issue_per_draw(est: str) -> float:
@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work of the cpu_baseline sample")
+    ap.add_argument("--tto-draws", type=int, default=W.DRAWS["C3"],
+                    help="draws/design of the time-to-optimal-design run (C3 slice); 0 = skip")
     return ap.parse_args()
 
 
@@ -246,6 +248,10 @@ def run_ours(args):
             "peak_basis": "128 lane-instr/clk/SM x SMs x sm_max_mhz (DESIGN.md §4)",
             "draws_per_s_kernel": draws_launch / (kms * 1e-3) * world}
 
+    tto = None
+    if args.tto_draws > 0:
+        tto = time_to_optimal_design(args, mc, torch, dist, world, rank, local, est)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, specs, alpha, pod, seconds=args.cpu_seconds)
@@ -261,12 +267,44 @@ def run_ours(args):
                            "l2": "no flush: the per-step TPS plan read (~%.1f GB) exceeds L2" % (
                                8.0 * sum((pod == k).sum() ** 2 for k in range(len(specs))) / 1e9)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "time_to_optimal_design": tto,
                 "clocks": clk,
                 "prep_s": {"candidates": round(t_cand, 3), "tps_plan": round(t_plan, 3)},
                 "best_design_first_problem": int(out[0][0].item())}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_to_optimal_design(args, mc, torch, dist, world, rank, local, est):
+    """BASELINE metric 2: wall-clock from the problem statement to the optimal design on the host,
+    for the C3 headline slice (scenario (c), r = (1, .45, .15), every valid m = 64 alpha design) at
+    `tto_draws` draws per design sharded over the ranks: candidates (GPU alpha_n solve) -> design
+    init -> TPS plan -> fused MC -> all_reduce -> finalize -> TPS+GCV -> argmax -> host."""
+    spec = W.c2_slice()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prob = mc.problem_formula10(spec.r, spec.delta0(), spec.i3, spec.alpha0)
+    alpha, pod = mc.candidates([prob], m=W.GRID_M, n3=0, seed=W.SEED, device=local)
+    dsg = mc.Design([prob], alpha, pod, seed=W.SEED, estimator=est, device=local)
+    dsg.smooth_plan()
+    res = mc.evaluate_design_objective(dsg, args.tto_draws, lam=-1.0, rank=rank, world=world)
+    best, val = res.best
+    t1 = time.perf_counter()
+    tt = torch.tensor([t1 - t0], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    raw = res.mean.cpu().numpy()
+    se = np.sqrt(res.var.cpu().numpy() / args.tto_draws)
+    out = {"seconds": float(tt[0]), "workload": "C3 slice: scenario (c), r=(1,0.45,0.15), all valid m=64 designs",
+           "designs": int(dsg.D), "draws_per_design": int(args.tto_draws), "n_gpus": world,
+           "best_design": int(best), "best_alpha": [float(x) for x in alpha[best]], "P_smoothed": float(val),
+           "P_hat": float(raw[best]), "SE": float(se[best]), "raw_argmax": int(np.argmax(raw)),
+           "lambda": float(res.lam_used.cpu().numpy()[0])}
+    dsg.close()
+    return out
 
 
 # ----------------------------------------------------------------------------------------------

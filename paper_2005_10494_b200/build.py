@@ -32,9 +32,11 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+    if not force and not needs_build() and "MC_LIB_OUT" not in os.environ:
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB, *sources(), "-lcusolver", "-lcublas"]
+    out = os.environ.get("MC_LIB_OUT", LIB)
+    extra = os.environ.get("MC_EXTRA_FLAGS", "").split()
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", out, *sources(), "-lcusolver", "-lcublas"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -161,25 +161,24 @@ __device__ __forceinline__ void box_muller_scaled(uint32_t wr, uint32_t wa, uint
   n1 = mr * sin_approx(x);
 }
 
-// Upper normal tail q = Phi(-a) = erfc(a/sqrt2)/2 for a >= 0 (Press et al., Numerical Recipes,
-// erfcc: t = 1/(1 + z/2), erfc(z) = t exp(-z^2 + poly(t)), fractional error < 1.2e-7), with the
-// exponent's constants pre-multiplied by log2(e) and the 1/2 folded in (EX2 on MUFU).
-// Returns q and e = 1 - q (= Phi(a)) without cancellation for either sign of a.
+// Upper normal tail q = Phi(-a) for a >= 0 in the Numerical-Recipes erfc form (Press et al., "erfcc":
+// t = 1/(1 + kappa a), q = t exp(-a^2/2 + poly(t))) refitted in base 2 with a degree-8 polynomial
+// (tools/fit_normal_tail.py: kappa = 0.4/sqrt2, max relative error 9.2e-8 in exact arithmetic): one RCP,
+// eight FFMAs, one EX2 on the MUFU pipe.  Returns q and e = 1 - q (= Phi(a)) without cancellation for
+// either sign of a.
 __device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
   const float aa = fabsf(a);
-  const float t = rcp_approx(fmaf(aa, 0.353553390593f, 1.0f));
-  constexpr double L2E = 1.4426950408889634;   // log2(e)
-  float p = (float)(0.17087277 * L2E);
-  p = fmaf(p, t, (float)(-0.82215223 * L2E));
-  p = fmaf(p, t, (float)(1.48851587 * L2E));
-  p = fmaf(p, t, (float)(-1.13520398 * L2E));
-  p = fmaf(p, t, (float)(0.27886807 * L2E));
-  p = fmaf(p, t, (float)(-0.18628806 * L2E));
-  p = fmaf(p, t, (float)(0.09678418 * L2E));
-  p = fmaf(p, t, (float)(0.37409196 * L2E));
-  p = fmaf(p, t, (float)(1.00002368 * L2E));
-  p = fmaf(p, t, (float)(-1.26551223 * L2E - 1.0));   // the -1 is the 1/2 of Phi = erfc/2
-  const float ex = ex2_approx(fmaf(aa * aa, (float)(-0.5 * L2E), p));   // -z^2 log2e, z = a/sqrt2
+  const float t = rcp_approx(fmaf(aa, 0.282842712474619f, 1.0f));
+  float p = -0.3020209548193252f;
+  p = fmaf(p, t, 1.3475361161107364f);
+  p = fmaf(p, t, -2.173205689641004f);
+  p = fmaf(p, t, 1.4767906809187563f);
+  p = fmaf(p, t, -0.6654844086664139f);
+  p = fmaf(p, t, 0.4449553247379003f);
+  p = fmaf(p, t, 0.5735953408558541f);
+  p = fmaf(p, t, 1.4456196577402736f);
+  p = fmaf(p, t, -3.1477861996521375f);
+  const float ex = ex2_approx(fmaf(aa * aa, -0.72134752044448170f, p));   // -a^2 log2(e) / 2
   const float qp = t * ex;                     // Phi(-|a|)
   const float qc = 1.0f - qp;                  // Phi(|a|)
   const bool pos = a >= 0.0f;
@@ -235,9 +234,40 @@ __device__ __forceinline__ float normal_quantile(float p, float pc) {
 }
 
 // normal_quantile() with sqrt(2) folded into the polynomial coefficients (one FMUL less).
+#ifndef MC_QUANTILE_BRANCHFREE
+#define MC_QUANTILE_BRANCHFREE 1
+#endif
 __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
   constexpr double S2 = 1.4142135623730950488;
   const float w = -0.69314718056f * (lg2_approx(fmaxf(p * pc, 1.0e-38f)) + 2.0f);
+#if MC_QUANTILE_BRANCHFREE
+  // all three polynomials with selects: one basic block (the scheduler can interleave across draws)
+  const float ww = w - 2.5f;
+  float g = (float)(2.81022636e-08 * S2);
+  g = fmaf(g, ww, (float)(3.43273939e-07 * S2));
+  g = fmaf(g, ww, (float)(-3.5233877e-06 * S2));
+  g = fmaf(g, ww, (float)(-4.39150654e-06 * S2));
+  g = fmaf(g, ww, (float)(0.00021858087 * S2));
+  g = fmaf(g, ww, (float)(-0.00125372503 * S2));
+  g = fmaf(g, ww, (float)(-0.00417768164 * S2));
+  g = fmaf(g, ww, (float)(0.246640727 * S2));
+  g = fmaf(g, ww, (float)(1.50140941 * S2));
+  const float sw = sqrt_approx(fminf(w, 88.0f));
+  const bool deep = w >= 16.0f;
+  // tail and deep tail share one Horner chain with selected coefficients
+  const float wt = deep ? sw - 6.0f : sw - 3.0f;
+  float gt = deep ? 0.0f : (float)(-0.000200214257 * S2);
+  gt = fmaf(gt, wt, deep ? 0.0f : (float)(0.000100950558 * S2));
+  gt = fmaf(gt, wt, deep ? (float)(7.926354328446905e-07 * S2) : (float)(0.00134934322 * S2));
+  gt = fmaf(gt, wt, deep ? (float)(-6.932396900083404e-06 * S2) : (float)(-0.00367342844 * S2));
+  gt = fmaf(gt, wt, deep ? (float)(2.5214179913746193e-05 * S2) : (float)(0.00573950773 * S2));
+  gt = fmaf(gt, wt, deep ? (float)(-3.964155257563107e-05 * S2) : (float)(-0.0076224613 * S2));
+  gt = fmaf(gt, wt, deep ? (float)(-0.0004801170143764466 * S2) : (float)(0.00943887047 * S2));
+  gt = fmaf(gt, wt, deep ? (float)(1.0096029043197632 * S2) : (float)(1.00167406 * S2));
+  gt = fmaf(gt, wt, deep ? (float)(5.859915256500244 * S2) : (float)(2.83297682 * S2));
+  g = w < 5.0f ? g : gt;
+  return g * (p - pc);
+#else
   float g;
   if (w < 5.0f) {
     const float ww = w - 2.5f;
@@ -275,6 +305,7 @@ __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
     }
   }
   return g * (p - pc);
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -22,7 +22,17 @@ constexpr int OFF_OB = 96;               // COND odd stage j: right-neighbour co
 constexpr int OFF_BSC = 101;             // row scale of b' = b * bsc (dump only)
 constexpr int SAMPLES_PER_THREAD = 128;  // per-thread sample run inside a warp tile (< 512: u32 sums)
 constexpr int MAX_BLOCK = 256;           // fused kernel __launch_bounds__
-constexpr int MIN_BLOCKS = 4;            // ... and min resident blocks per SM (register cap 64)
+#ifndef MC_PIPELINE
+#define MC_PIPELINE 0
+#endif
+#ifndef MC_MIN_BLOCKS_COND
+#define MC_MIN_BLOCKS_COND 4
+#endif
+#ifndef MC_MIN_BLOCKS_IND
+#define MC_MIN_BLOCKS_IND 5
+#endif
+constexpr int MIN_BLOCKS_COND = MC_MIN_BLOCKS_COND;   // min resident 256-thread blocks per SM, n <= 3
+constexpr int MIN_BLOCKS_IND = MC_MIN_BLOCKS_IND;     //   (register caps 64 / 48)
 
 void set_error(const std::string& msg);
 mc_status cuda_fail(cudaError_t e, const char* where);

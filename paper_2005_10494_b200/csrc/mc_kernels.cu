@@ -59,6 +59,29 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
   static_assert(SAMPLES_PER_THREAD % G::L == 0, "L must divide the per-thread run");
   uint64_t q = s_begin * (uint64_t)G::U / 4;   // first Philox block of this thread's run
   const uint32_t one = one_bits_reg();
+#if MC_PIPELINE
+  if constexpr (!MASKED) {
+    // software-pipelined: the next step's Philox words are generated while this step's draws are
+    // evaluated (independent instruction streams the scheduler can interleave across pipes)
+    uint32_t w[G::BLOCKS * 4];
+#pragma unroll
+    for (int b = 0; b < G::BLOCKS; ++b) philox_block_rk(q + b, lo1d, hi1d, rk, &w[4 * b]);
+    q += G::BLOCKS;
+#pragma unroll 2
+    for (int st = 0; st < STEPS; ++st) {
+      uint32_t wn[G::BLOCKS * 4];
+#pragma unroll
+      for (int b = 0; b < G::BLOCKS; ++b) philox_block_rk(q + b, lo1d, hi1d, rk, &wn[4 * b]);
+      q += G::BLOCKS;
+#pragma unroll
+      for (int l = 0; l < G::L; ++l) accumulate<EST>(draw_utility<N, EST, false>(&w[l * G::U], one, zc, pr), a1, a2);
+#pragma unroll
+      for (int k = 0; k < G::BLOCKS * 4; ++k) w[k] = wn[k];
+    }
+    if constexpr (EST == 1) a2 = a1;
+    return;
+  }
+#endif
 #pragma unroll 1
   for (int st = 0; st < STEPS; ++st) {
     const uint64_t s0 = s_begin + (uint64_t)st * G::L;
@@ -83,10 +106,12 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
 // Work unit = one WARP tile: (design, 32 x SAMPLES_PER_THREAD consecutive samples).  Warps are
 // independent (no block barrier): each reduces its tile with 64-bit shuffles and lane 0 issues one
 // 64-bit atomicAdd pair.  Warp tiles are strided over the persistent grid's warps.
-constexpr int min_blocks(int n) { return n <= 3 ? MIN_BLOCKS : (n <= 5 ? 2 : 1); }
+constexpr int min_blocks(int n, int est) {
+  return n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1);
+}
 
 template <int N, int EST>
-__global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N)) mc_fused_kernel(
+__global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST)) mc_fused_kernel(
     const float* __restrict__ prob, const float* __restrict__ zc_all, const int32_t* __restrict__ pod, int64_t d0,
     uint64_t B, uint64_t E, uint64_t Balign, int64_t tiles_per_design, int64_t total_tiles, const RoundKeys rk,
     unsigned long long* __restrict__ sums) {

@@ -38,17 +38,18 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    return os.environ.get("MC_LIB_PATH", _build.LIB)
 
 
 def lib() -> ctypes.CDLL:
     """Load the in-tree library (raises if it has not been built)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_build.LIB):
-            raise RuntimeError(f"{_build.LIB} is missing: run `python -m paper_2005_10494_b200.build` "
+        path = lib_path()
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: run `python -m paper_2005_10494_b200.build` "
                                "(no CPU fallback exists)")
-        L = ctypes.CDLL(_build.LIB)
+        L = ctypes.CDLL(path)
         i32, i64, u64, d, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
         P = ctypes.POINTER
         L.mc_last_error.restype = ctypes.c_char_p
