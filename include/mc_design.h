@@ -42,7 +42,9 @@ typedef enum {
 } mc_estimator;
 
 /* One fixed-r design problem: nested fractions r, information units I3 (Eq. 9),
- * FWER budget alpha0 (Formula 2) and the Gaussian effect prior f(Delta) (Formula 10).
+ * FWER budget alpha0 (Formula 2) and the effect prior f(Delta): model 0 = Gaussian (Formula 10 or a
+ * general Cholesky factor), model 1 = the C4 strata prior (n = 2, see
+ * mc_problem_strata).
  *   r[0] = 1 > r[1] > ... > r[n-1] > 0 with r[i+1]/r[i] <= 1 - 1e-6 (S:32 guard);
  *   0 < alpha0 < 0.5; i3 > 0.
  *   Prior: Delta ~ N(theta, Sigma_p).  has_prior_chol = 0: Sigma_p = diag(sigma) Sigma0 diag(sigma)
@@ -58,6 +60,10 @@ typedef struct {
     double  theta[MC_MAX_N];
     double  sigma[MC_MAX_N];
     double  prior_chol[MC_MAX_N * MC_MAX_N];
+    int32_t model;            /* 0 = Gaussian prior, 1 = C4 strata prior */
+    int32_t reserved;
+    double  strata[10];       /* model 1: (mean, sd) of logit prevalence, effect+, effect-, log variance
+                                 inflation, logit dropout */
 } mc_problem;
 
 typedef struct mc_ctx mc_ctx;
@@ -77,6 +83,14 @@ double mc_threshold(double alpha);
  * MC_ERR_INVALID if r or delta0 violate their invariants. */
 mc_status mc_problem_formula10(int32_t n, const double* r, const double* delta0, double i3,
                                double alpha0, mc_problem* out);
+
+/* C4 strata prior (a synthetic extension of Formula 3 — not in the paper): n = 2,
+ * r = (1, r2), 0 < r2 < 1; five independent normal components per draw with (mean, sd) pairs
+ * strata[10] = (logit pi, delta+, delta-, log v, logit d).  Per draw: I_eff = I3 (1 - d)/v,
+ * q+ = min(1, pi/r2), q- = max(0, (pi - r2)/(1 - r2)), Delta_2 = q+ delta+ + (1-q+) delta-,
+ * Delta_neg = q- delta+ + (1-q-) delta-, Delta_1 = r2 Delta_2 + (1-r2) Delta_neg, mu_i = sqrt(r_i I_eff) Delta_i.
+ * MC_ERR_INVALID if r2 or a standard deviation is out of range. */
+mc_status mc_problem_strata(double r2, double i3, double alpha0, const double* strata, mc_problem* out);
 
 /* ---- a1: candidate designs ------------------------------------- */
 

@@ -173,34 +173,22 @@ int or_words_per_draw(int n, int p, int est)
     return 2 * ((p + n + 1) / 2);
 }
 
-double or_draw(int n, int p, const double *r, double i3, const double *theta, const double *Lp,
-               const double *z, int est, uint64_t seed, uint32_t design, uint64_t s,
-               double *eps_out, double *delta_out, double *b_out, double *wnull_out)
+/* Box-Muller: pair j uses words 2j (radius) and 2j+1 (angle) of the draw. */
+static void bm_normals(uint64_t seed, uint32_t design, uint64_t w0, int nnorm, double *normals)
 {
-    const int U = or_words_per_draw(n, p, est);
-    const uint64_t w0 = s * (uint64_t)U;
-    const int nnorm = (est == 0) ? p : p + n;
-    double normals[2 * OR_MAXN + 2];
-    /* Box-Muller: pair j uses words 2j (radius) and 2j+1 (angle). */
     for (int j = 0; 2 * j < nnorm; ++j) {
         double R = sqrt(-2.0 * log(u_radius(or_word(seed, design, w0 + 2 * j))));
         double a = 2.0 * M_PI * u_angle(or_word(seed, design, w0 + 2 * j + 1));
         normals[2 * j] = R * cos(a);
         normals[2 * j + 1] = R * sin(a);
     }
-    /* Formula 10: Delta = theta + Lp * eps. */
-    double delta[OR_MAXN], b[OR_MAXN];
-    for (int i = 0; i < n; ++i) {
-        double acc = theta[i];
-        for (int k = 0; k <= i && k < p; ++k) acc += Lp[i * p + k] * normals[k];
-        delta[i] = acc;
-    }
-    /* Formulas 3-5: thresholds of Phi_Sigma0 are z_i - sqrt(r_i I3) Delta_i. */
-    for (int i = 0; i < n; ++i) b[i] = z[i] - sqrt(r[i] * i3) * delta[i];
-    if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
-    if (delta_out) for (int i = 0; i < n; ++i) delta_out[i] = delta[i];
-    if (b_out) for (int i = 0; i < n; ++i) b_out[i] = b[i];
+}
 
+/* Utility of one draw given the thresholds b of Phi_Sigma0 (Formulas 4-7):
+ * IND uses the null normals w[0..n); COND reads its uniforms at word vw0 + a. */
+static double utility_from_b(int n, const double *r, const double *b, const double *w, int est,
+                             uint64_t seed, uint32_t design, uint64_t vw0, double *wnull_out)
+{
     double S0[OR_MAXN * OR_MAXN], L0[OR_MAXN * OR_MAXN];
     or_null_corr(n, r, S0);
     if (or_cholesky(n, S0, L0) != 0) return NAN;
@@ -211,7 +199,7 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
         int reject = 0;
         for (int i = 0; i < n; ++i) {
             double x = 0.0;
-            for (int k = 0; k <= i; ++k) x += L0[i * n + k] * normals[p + k];
+            for (int k = 0; k <= i; ++k) x += L0[i * n + k] * w[k];
             if (wnull_out) wnull_out[i] = x;
             if (x > b[i]) reject = 1;
         }
@@ -225,7 +213,6 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
      * Only the first n/2 (even-population) stages draw a uniform v_a: A.1 makes X a Markov chain,
      * so every odd population is independent of the other odd ones given the even ones, i.e.
      * L'_aj = 0 for j >= n/2 (checked below) and those y_j are never used.               */
-    const int vbase = 2 * ((p + 1) / 2);
     const int neven = n / 2;
     int ord[OR_MAXN], k = 0;
     for (int i = 1; i < n; i += 2) ord[k++] = i;     /* 0-based index of population 2, 4, ... */
@@ -248,11 +235,87 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
         prod *= e;
         if (prod == 0.0) break;                        /* u = 1 exactly; later stages are irrelevant */
         if (a < neven) {
-            double v = u_open(or_word(seed, design, w0 + vbase + a));
+            double v = u_open(or_word(seed, design, vw0 + a));
             y[a] = or_Phi_inv(v * e);
         }
     }
     return 1.0 - prod;
+}
+
+
+double or_draw(int n, int p, const double *r, double i3, const double *theta, const double *Lp,
+               const double *z, int est, uint64_t seed, uint32_t design, uint64_t s,
+               double *eps_out, double *delta_out, double *b_out, double *wnull_out)
+{
+    const int U = or_words_per_draw(n, p, est);
+    const uint64_t w0 = s * (uint64_t)U;
+    const int nnorm = (est == 0) ? p : p + n;
+    double normals[2 * OR_MAXN + 2];
+    bm_normals(seed, design, w0, nnorm, normals);
+    /* Formula 10: Delta = theta + Lp * eps. */
+    double delta[OR_MAXN], b[OR_MAXN];
+    for (int i = 0; i < n; ++i) {
+        double acc = theta[i];
+        for (int k = 0; k <= i && k < p; ++k) acc += Lp[i * p + k] * normals[k];
+        delta[i] = acc;
+    }
+    /* Formulas 3-5: thresholds of Phi_Sigma0 are z_i - sqrt(r_i I3) Delta_i. */
+    for (int i = 0; i < n; ++i) b[i] = z[i] - sqrt(r[i] * i3) * delta[i];
+    if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
+    if (delta_out) for (int i = 0; i < n; ++i) delta_out[i] = delta[i];
+    if (b_out) for (int i = 0; i < n; ++i) b_out[i] = b[i];
+    return utility_from_b(n, r, b, normals + p, est, seed, design, w0 + 2 * ((p + 1) / 2), wnull_out);
+}
+
+/* C4 strata prior (a synthetic extension inside the Formula-3 model, not in the paper).
+ * n = 2 (overall population and a biomarker-positive subset of fraction r2), five independent normal
+ * components per draw, sp[10] = (mean, sd) of: logit prevalence pi, effect in responders delta+,
+ * effect in non-responders delta-, log variance inflation v, logit dropout d.
+ *   I_eff = I3 (1 - d) / v;  responders are the top-pi biomarker fraction:
+ *   q+ = min(1, pi / r2), q- = max(0, (pi - r2) / (1 - r2));
+ *   Delta_2 = q+ delta+ + (1 - q+) delta-,  Delta_neg = q- delta+ + (1 - q-) delta-,
+ *   Delta_1 = r2 Delta_2 + (1 - r2) Delta_neg;  mu_i = sqrt(r_i I_eff) Delta_i;  b = z - mu.      */
+double or_draw_strata(double r2, double i3, const double *sp, const double *z, int est, uint64_t seed,
+                      uint32_t design, uint64_t s, double *eps_out, double *delta_out, double *b_out,
+                      double *wnull_out)
+{
+    const int n = 2, p = 5;
+    const double r[2] = { 1.0, r2 };
+    const int U = or_words_per_draw(n, p, est);
+    const uint64_t w0 = s * (uint64_t)U;
+    double normals[2 * OR_MAXN + 2];
+    bm_normals(seed, design, w0, est == 0 ? p : p + n, normals);
+    const double pi = 1.0 / (1.0 + exp(-(sp[0] + sp[1] * normals[0])));
+    const double dp = sp[2] + sp[3] * normals[1];
+    const double dm = sp[4] + sp[5] * normals[2];
+    const double v = exp(sp[6] + sp[7] * normals[3]);
+    const double d = 1.0 / (1.0 + exp(-(sp[8] + sp[9] * normals[4])));
+    const double ieff = i3 * (1.0 - d) / v;
+    const double qp = fmin(1.0, pi / r2);
+    const double qm = fmax(0.0, (pi - r2) / (1.0 - r2));
+    const double d2 = qp * dp + (1.0 - qp) * dm;
+    const double dneg = qm * dp + (1.0 - qm) * dm;
+    const double d1 = r2 * d2 + (1.0 - r2) * dneg;
+    double b[2];
+    b[0] = z[0] - sqrt(r[0] * ieff) * d1;
+    b[1] = z[1] - sqrt(r[1] * ieff) * d2;
+    if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
+    if (delta_out) { delta_out[0] = d1; delta_out[1] = d2; }
+    if (b_out) { b_out[0] = b[0]; b_out[1] = b[1]; }
+    return utility_from_b(n, r, b, normals + p, est, seed, design, w0 + 2 * ((p + 1) / 2), wnull_out);
+}
+
+void or_design_sums_strata(double r2, double i3, const double *sp, const double *z, int est, uint64_t seed,
+                           uint32_t design, uint64_t s0, uint64_t count, int64_t *sums)
+{
+    int64_t a1 = 0, a2 = 0;
+    for (uint64_t s = s0; s < s0 + count; ++s) {
+        double u = or_draw_strata(r2, i3, sp, z, est, seed, design, s, NULL, NULL, NULL, NULL);
+        a1 += (int64_t)nearbyint(ldexp(u, 23));
+        a2 += (int64_t)nearbyint(ldexp(u * u, 23));
+    }
+    sums[0] += a1;
+    sums[1] += a2;
 }
 
 /* Per-design sums over samples [s0, s0+count): each draw's u

@@ -63,6 +63,9 @@ def lib():
         L.or_alpha_grid.argtypes = [i32, P(d), d, i32, d, P(d), P(ctypes.c_uint8)]
         L.or_alpha_grid.restype = i64
         L.or_subset.argtypes = [i64, i64, u64, P(i64)]
+        L.or_draw_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u64, P(d), P(d), P(d), P(d)]
+        L.or_draw_strata.restype = d
+        L.or_design_sums_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u64, u64, P(i64)]
         _lib = L
     return _lib
 
@@ -393,3 +396,77 @@ def argmax(values) -> int:
         if v[i] > v[best]:
             best = i
     return best
+
+
+# --------------------------------------------------------------------------------------
+# C4: 5-D strata prior (synthetic extension of Formula 3, see oracle.c)
+
+def draw_strata(r2: float, i3: float, sp, alpha, est: int, seed: int, design: int, s: int) -> dict:
+    z = thresholds(alpha)
+    eps, delta, b, wn = np.zeros(5), np.zeros(2), np.zeros(2), np.zeros(2)
+    P = ctypes.POINTER(ctypes.c_double)
+    u = lib().or_draw_strata(float(r2), float(i3), _dp(np.asarray(sp, dtype=np.float64)), _dp(z), est, seed, design,
+                             s, eps.ctypes.data_as(P), delta.ctypes.data_as(P), b.ctypes.data_as(P),
+                             wn.ctypes.data_as(P))
+    return {"u": float(u), "eps": eps, "delta": delta, "b": b, "xnull": wn}
+
+
+def design_sums_strata(r2: float, i3: float, sp, alpha, est: int, seed: int, design: int, s0: int,
+                       count: int) -> np.ndarray:
+    z = thresholds(alpha)
+    sums = np.zeros(2, dtype=np.int64)
+    lib().or_design_sums_strata(float(r2), float(i3), _dp(np.asarray(sp, dtype=np.float64)), _dp(z), est, seed,
+                                design, s0, count, sums.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    return sums
+
+
+def strata_b(r2: float, i3: float, sp, z, e):
+    """Deterministic map (eps_1..eps_5) -> b of the C4 model (same formulas as oracle.c, vectorised)."""
+    e = np.asarray(e, dtype=np.float64)
+    pi = 1.0 / (1.0 + np.exp(-(sp[0] + sp[1] * e[..., 0])))
+    dp = sp[2] + sp[3] * e[..., 1]
+    dm = sp[4] + sp[5] * e[..., 2]
+    v = np.exp(sp[6] + sp[7] * e[..., 3])
+    d = 1.0 / (1.0 + np.exp(-(sp[8] + sp[9] * e[..., 4])))
+    ieff = i3 * (1.0 - d) / v
+    qp = np.minimum(1.0, pi / r2)
+    qm = np.maximum(0.0, (pi - r2) / (1.0 - r2))
+    d2 = qp * dp + (1.0 - qp) * dm
+    dneg = qm * dp + (1.0 - qm) * dm
+    d1 = r2 * d2 + (1.0 - r2) * dneg
+    return np.stack([z[0] - np.sqrt(ieff) * d1, z[1] - np.sqrt(r2 * ieff) * d2], axis=-1)
+
+
+def assurance_strata_quadrature(r2: float, i3: float, sp, alpha, n_gh: int = 8, n_gl: int = 24) -> float:
+    """Tensor-product brute force of Formula 4 under the C4 prior: Gauss-Hermite over the four smooth
+    components and Gauss-Legendre on each side of the prevalence kink eps1* = (logit r2 - mu)/sd (where
+    q+ = min(1, pi/r2) bends), inner Phi_Sigma0 by the exact bivariate orthant."""
+    z = thresholds(alpha)
+    xh, wh = np.polynomial.hermite_e.hermegauss(n_gh)
+    wh = wh / wh.sum()
+    kink = (np.log(r2 / (1 - r2)) - sp[0]) / sp[1] if sp[1] > 0 else None
+    xg, wg = np.polynomial.legendre.leggauss(n_gl)
+    if kink is None:
+        e1 = np.array([0.0]); w1 = np.array([1.0])
+    else:
+        lo, hi = -9.0, 9.0
+        segs = [(lo, min(max(kink, lo), hi)), (min(max(kink, lo), hi), hi)]
+        e1, w1 = [], []
+        for a, b in segs:
+            if b <= a:
+                continue
+            x = 0.5 * (b - a) * (xg + 1) + a
+            e1.append(x)
+            w1.append(0.5 * (b - a) * wg * np.exp(-0.5 * x * x) / np.sqrt(2 * np.pi))
+        e1 = np.concatenate(e1); w1 = np.concatenate(w1)
+    total = 0.0
+    r = [1.0, r2]
+    for i1, a1 in enumerate(e1):
+        for i2 in range(n_gh):
+            for i3_ in range(n_gh):
+                for i4 in range(n_gh):
+                    for i5 in range(n_gh):
+                        e = np.array([a1, xh[i2], xh[i3_], xh[i4], xh[i5]])
+                        b = strata_b(r2, i3, sp, z, e)
+                        total += w1[i1] * wh[i2] * wh[i3_] * wh[i4] * wh[i5] * (1.0 - mvn_orthant(r, b))
+    return float(total)

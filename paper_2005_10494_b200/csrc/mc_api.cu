@@ -76,6 +76,13 @@ static mc_status validate_problem(const mc_problem& p, int idx) {
     return MC_ERR_INVALID;
   };
   if (p.n < 1 || p.n > MC_MAX_N) return bad("n must be in [1, 10] (P:47)");
+  if (p.model != 0 && p.model != 1) return bad("model must be 0 (Gaussian prior) or 1 (C4 strata prior)");
+  if (p.model == 1) {
+    if (p.n != 2) return bad("the C4 strata prior has n = 2");
+    for (int k = 0; k < 10; ++k)
+      if (!std::isfinite(p.strata[k]) || (k % 2 == 1 && !(p.strata[k] >= 0.0)))
+        return bad("strata parameters must be finite with sd >= 0");
+  }
   if (p.r[0] != 1.0) return bad("r[0] must be exactly 1 (P:47: 1 = r_1 > r_2 > ...)");
   for (int i = 0; i + 1 < p.n; ++i) {
     if (!(p.r[i + 1] > 0.0) || !(p.r[i + 1] < p.r[i])) return bad("r must be strictly decreasing and > 0 (P:47)");
@@ -83,12 +90,12 @@ static mc_status validate_problem(const mc_problem& p, int idx) {
   }
   if (!(p.alpha0 > 0.0 && p.alpha0 < 0.5)) return bad("alpha0 must be in (0, 0.5) (Formula 2)");
   if (!(p.i3 > 0.0) || !std::isfinite(p.i3)) return bad("i3 must be finite and > 0 (Eq. 9)");
-  for (int i = 0; i < p.n; ++i) {
+  for (int i = 0; i < p.n && p.model == 0; ++i) {
     if (!std::isfinite(p.theta[i])) return bad("theta must be finite (Formula 10)");
     if (!p.has_prior_chol && !(p.sigma[i] >= 0.0 && std::isfinite(p.sigma[i])))
       return bad("sigma must be finite and >= 0 (Formula 10)");
   }
-  if (p.has_prior_chol) {
+  if (p.has_prior_chol && p.model == 0) {
     for (int i = 0; i < p.n; ++i) {
       if (!(p.prior_chol[i * MC_MAX_N + i] >= 0.0)) return bad("prior_chol diagonal must be >= 0");
       for (int j = 0; j <= i; ++j)
@@ -201,6 +208,21 @@ static void problem_record(const mc_problem& p, int est, float* rec) {
     rec[OFF_OA + j] = (float)(sc.oa[j] / sc.sd[2 * j]);
     rec[OFF_OB + j] = (float)(sc.ob[j] / sc.sd[2 * j]);
   }
+  if (p.model == 1) {
+    // C4 strata prior: the kernel draws eps / BM_K, so every sd carries BM_K
+    float* r = rec + OFF_STR;
+    for (int k = 0; k < 10; ++k) r[k] = (float)(k % 2 == 1 ? BM_K * p.strata[k] : p.strata[k]);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j <= i; ++j) rec[OFF_M + i * (i + 1) / 2 + j] = 0.0f;
+    const double r2 = p.r[1];
+    r[10] = (float)p.i3;
+    r[11] = (float)(1.0 / r2);
+    r[12] = (float)(1.0 / (1.0 - r2));
+    r[13] = (float)r2;
+    r[14] = (float)std::sqrt(r2);
+    r[15] = (float)row_scale(p, est, 0);
+    r[16] = (float)row_scale(p, est, 1);
+  }
 }
 
 }  // namespace mci
@@ -250,6 +272,23 @@ mc_status mc_problem_formula10(int32_t n, const double* r, const double* delta0,
   return MC_OK;
 }
 
+mc_status mc_problem_strata(double r2, double i3, double alpha0, const double* strata, mc_problem* out) {
+  if (!out || !strata) { set_error("mc_problem_strata: null pointer"); return MC_ERR_INVALID; }
+  mc_problem p;
+  std::memset(&p, 0, sizeof p);
+  p.n = 2;
+  p.model = 1;
+  p.i3 = i3;
+  p.alpha0 = alpha0;
+  p.r[0] = 1.0;
+  p.r[1] = r2;
+  for (int k = 0; k < 10; ++k) p.strata[k] = strata[k];
+  mc_status s = validate_problem(p, 0);
+  if (s != MC_OK) return s;
+  *out = p;
+  return MC_OK;
+}
+
 mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs, const double* alpha,
                          const int32_t* pod, int64_t D, uint64_t seed, int32_t estimator, int32_t device) {
   if (!ctx || !probs || n_probs <= 0 || D < 0 || (D > 0 && (!alpha || !pod))) {
@@ -268,8 +307,8 @@ mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs,
   for (int k = 0; k < n_probs; ++k) {
     mc_status s = validate_problem(probs[k], k);
     if (s != MC_OK) return s;
-    if (probs[k].n != n) {
-      set_error("mc_design_init: all problems must share n");
+    if (probs[k].n != n || probs[k].model != probs[0].model) {
+      set_error("mc_design_init: all problems must share n and the prior model");
       return MC_ERR_INVALID;
     }
   }
@@ -299,6 +338,7 @@ mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs,
   c->device = device;
   c->n = n;
   c->est = estimator;
+  c->model = probs[0].model;
   c->n_probs = n_probs;
   c->D = D;
   c->seed = seed;
@@ -312,7 +352,8 @@ mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs,
   std::vector<double> ctheta((size_t)n_probs * n * 2);
   for (int k = 0; k < n_probs; ++k)
     for (int i = 0; i < n; ++i) {
-      ctheta[((size_t)k * n + i) * 2] = std::sqrt(probs[k].r[i] * probs[k].i3) * probs[k].theta[i];
+      ctheta[((size_t)k * n + i) * 2] =
+          probs[k].model == 1 ? 0.0 : std::sqrt(probs[k].r[i] * probs[k].i3) * probs[k].theta[i];
       ctheta[((size_t)k * n + i) * 2 + 1] = row_scale(probs[k], estimator, i);
     }
   auto fail = [&](cudaError_t e, const char* w) { mc_status s = cuda_fail(e, w); mc_destroy(c); return s; };
@@ -437,8 +478,8 @@ mc_status mc_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, 
 
 int64_t mc_num_designs(const mc_ctx* c) { return c ? c->D : -1; }
 int32_t mc_num_problems(const mc_ctx* c) { return c ? c->n_probs : -1; }
-int32_t mc_words_per_draw(const mc_ctx* c) { return c ? words_per_draw(c->n, c->est) : -1; }
-int32_t mc_draw_dump_stride(const mc_ctx* c) { return c ? draw_dump_stride(c->n, c->est) : -1; }
+int32_t mc_words_per_draw(const mc_ctx* c) { return c ? words_per_draw(c->n, c->est, c->model) : -1; }
+int32_t mc_draw_dump_stride(const mc_ctx* c) { return c ? draw_dump_stride(c->n, c->est, c->model) : -1; }
 int64_t mc_kernel_launches(const mc_ctx* c) { return c ? c->launches : -1; }
 
 mc_status mc_philox_dump(uint64_t seed, const uint32_t* design, const uint64_t* word, int64_t count, uint32_t* out,

@@ -13,10 +13,11 @@ namespace mcd {
 
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
-// Geometry of one draw for N populations, prior dimension P = N, estimator EST (0 COND, 1 IND).
-template <int N, int EST>
+// Geometry of one draw for N populations, estimator EST (0 COND, 1 IND) and prior MODEL
+// (0: Gaussian, prior dimension P = N; 1: the C4 strata prior, P = 5, N = 2).
+template <int N, int EST, int MODEL = 0>
 struct Geo {
-  static constexpr int P = N;
+  static constexpr int P = MODEL == 1 ? 5 : N;
   static constexpr int NNORM = (EST == 0) ? P : P + N;          // normals per draw
   static constexpr int NPAIR = (NNORM + 1) / 2;                   // Box-Muller pairs
   static constexpr int U = (EST == 0) ? 2 * ((P + 1) / 2) + N / 2 : 2 * NPAIR;   // words per draw
@@ -329,21 +330,55 @@ struct ProbRegs {
 
 // One draw from its U words w[0..U): returns u in [0,1].  If DBG, writes the (unscaled) normals,
 // b and u; bsc[i] (the row scales) and BM_K undo the folding for the dump.
-template <int N, int EST, bool DBG>
+// C4 strata prior parameters (MODEL 1; mc_api.cu problem_record(): sds pre-multiplied by BM_K).
+struct StrataRegs {
+  float pm, ps, dpm, dps, dmm, dms, lvm, lvs, ldm, lds;   // (mean, sd) of the five components
+  float i3, inv_r2, inv_1mr2, r2, sqrt_r2, rs0, rs1;      // I3, 1/r2, 1/(1-r2), r2, sqrt(r2), row scales
+};
+
+// b = z - mu of the C4 strata model (oracle.c or_draw_strata) from the five scaled
+// normals: I_eff = I3 (1-d)/v; q+ = min(1, pi/r2), q- = max(0, (pi - r2)/(1 - r2));
+// Delta_2 = delta- + q+ (delta+ - delta-), Delta_neg = delta- + q- (delta+ - delta-),
+// Delta_1 = Delta_neg + r2 (Delta_2 - Delta_neg); mu_1 = sqrt(I_eff) Delta_1, mu_2 = sqrt(r2 I_eff) Delta_2.
+__device__ __forceinline__ void strata_b(const float* nrm, const float* zc, const StrataRegs& s, float* b) {
+  constexpr float L2E = 1.44269504088896341f;
+  const float pi = rcp_approx(1.0f + ex2_approx(-L2E * fmaf(s.ps, nrm[0], s.pm)));
+  const float dp = fmaf(s.dps, nrm[1], s.dpm);
+  const float dm = fmaf(s.dms, nrm[2], s.dmm);
+  const float inv_v = ex2_approx(-L2E * fmaf(s.lvs, nrm[3], s.lvm));
+  const float omd = rcp_approx(1.0f + ex2_approx(L2E * fmaf(s.lds, nrm[4], s.ldm)));   // 1 - d
+  const float si = sqrt_approx(s.i3 * omd * inv_v);
+  const float qp = fminf(1.0f, pi * s.inv_r2);
+  const float qm = fmaxf(0.0f, (pi - s.r2) * s.inv_1mr2);
+  const float dd = dp - dm;
+  const float d2 = fmaf(qp, dd, dm);
+  const float dneg = fmaf(qm, dd, dm);
+  const float d1 = fmaf(s.r2, d2 - dneg, dneg);
+  b[0] = fmaf(-si * s.rs0, d1, zc[0]);
+  b[1] = fmaf(-si * s.sqrt_r2 * s.rs1, d2, zc[1]);
+}
+
+template <int N, int EST, bool DBG, int MODEL = 0>
 __device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, const float* zc, const ProbRegs<N>& pr,
-                                              float* dbg = nullptr, const float* bsc = nullptr) {
-  using G = Geo<N, EST>;
+                                              float* dbg = nullptr, const float* bsc = nullptr,
+                                              const StrataRegs* sr = nullptr) {
+  using G = Geo<N, EST, MODEL>;
   float nrm[2 * G::NPAIR];
 #pragma unroll
   for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(w[2 * j], w[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
-  // b_i = z_i - c_i Delta_i = (z_i - c_i theta_i) - sum_{j<=i} (c_i L_p,ij) eps_j   (Formulas 3-5, 10)
   float b[N];
+  if constexpr (MODEL == 1) {
+    static_assert(N == 2, "the C4 strata model has n = 2");
+    strata_b(nrm, zc, *sr, b);
+  } else {
+    // b_i = z_i - c_i Delta_i = (z_i - c_i theta_i) - sum_{j<=i} (c_i L_p,ij) eps_j   (Formulas 3-5, 10)
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    float acc = zc[i];
+    for (int i = 0; i < N; ++i) {
+      float acc = zc[i];
 #pragma unroll
-    for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
-    b[i] = acc;
+      for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
+      b[i] = acc;
+    }
   }
   float u = 0.0f;
   if constexpr (EST == 1) {

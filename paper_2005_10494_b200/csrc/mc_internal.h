@@ -10,7 +10,7 @@
 
 namespace mci {
 
-constexpr int PROB_STRIDE = 112;         // floats per device problem record
+constexpr int PROB_STRIDE = 144;         // floats per device problem record
 constexpr int OFF_M = 0;                 // packed M = diag(c) L_p with the folded row scales (55 floats for n = 10)
 constexpr int OFF_RHO = 56;              // IND: rho_i = sqrt(r_{i+1}/r_i)
 constexpr int OFF_SD = 66;               // IND: s_i = sqrt(1 - rho_i^2)
@@ -20,11 +20,9 @@ constexpr int OFF_ESD = 86;              // COND even stage k: conditional sd_k
 constexpr int OFF_OA = 91;               // COND odd stage j: left-neighbour coefficient / gamma_j
 constexpr int OFF_OB = 96;               // COND odd stage j: right-neighbour coefficient / gamma_j
 constexpr int OFF_BSC = 101;             // row scale of b' = b * bsc (dump only)
+constexpr int OFF_STR = 112;             // C4 strata model: 17 floats (mc_device.cuh StrataRegs)
 constexpr int SAMPLES_PER_THREAD = 128;  // per-thread sample run inside a warp tile (< 512: u32 sums)
 constexpr int MAX_BLOCK = 256;           // fused kernel __launch_bounds__
-#ifndef MC_PIPELINE
-#define MC_PIPELINE 0
-#endif
 #ifndef MC_MIN_BLOCKS_COND
 #define MC_MIN_BLOCKS_COND 4
 #endif
@@ -61,6 +59,7 @@ struct mc_ctx {
   int device = 0;
   int n = 0;
   int est = 0;
+  int model = 0;                         // 0 Gaussian prior (Formula 10 / general), 1 C4 strata prior
   int32_t n_probs = 0;
   int64_t D = 0;
   uint64_t seed = 0;
@@ -92,8 +91,8 @@ mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64
                              uint32_t* out, cudaStream_t st);
 mc_status launch_draw_dump(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
                            cudaStream_t st);
-int draw_dump_stride(int n, int est);
-int words_per_draw(int n, int est);
+int draw_dump_stride(int n, int est, int model);
+int words_per_draw(int n, int est, int model);
 mc_status launch_zc(mc_ctx* c, cudaStream_t st);
 mc_status launch_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, cudaStream_t st);
 mc_status alpha_grid_solve(const mc_problem* probs, int32_t n_probs, int32_t m, int device,

@@ -41,6 +41,15 @@ __device__ __forceinline__ void load_problem(const float* __restrict__ rec, Prob
   }
 }
 
+__device__ __forceinline__ void load_strata(const float* __restrict__ rec, StrataRegs& sr) {
+  const float* r = rec + OFF_STR;
+  sr.pm = __ldg(r + 0); sr.ps = __ldg(r + 1); sr.dpm = __ldg(r + 2); sr.dps = __ldg(r + 3);
+  sr.dmm = __ldg(r + 4); sr.dms = __ldg(r + 5); sr.lvm = __ldg(r + 6); sr.lvs = __ldg(r + 7);
+  sr.ldm = __ldg(r + 8); sr.lds = __ldg(r + 9); sr.i3 = __ldg(r + 10); sr.inv_r2 = __ldg(r + 11);
+  sr.inv_1mr2 = __ldg(r + 12); sr.r2 = __ldg(r + 13); sr.sqrt_r2 = __ldg(r + 14); sr.rs0 = __ldg(r + 15);
+  sr.rs1 = __ldg(r + 16);
+}
+
 // fixed-point accumulation of one draw: q(x) = round-half-even(2^23 x) for x in [0,1] is the
 // mantissa of the fp32 sum x + 1 (one FADD / FFMA + one IADD3).  IND: u in {0, 1}, u^2 = u, so only
 // the first sum is accumulated (the second is copied at the end).
@@ -50,38 +59,15 @@ __device__ __forceinline__ void accumulate(float u, uint32_t& a1, uint32_t& a2) 
   if constexpr (EST == 0) a2 += __float_as_uint(fmaf(u, u, 1.0f)) - 0x3F800000u;
 }
 
-template <int N, int EST, bool MASKED>
+template <int N, int EST, bool MASKED, int MODEL>
 __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64_t E, uint32_t lo1d, uint32_t hi1d,
-                                            const RoundKeys& rk, const float* zc, const ProbRegs<N>& pr, uint32_t& a1,
-                                            uint32_t& a2) {
-  using G = Geo<N, EST>;
+                                            const RoundKeys& rk, const float* zc, const ProbRegs<N>& pr,
+                                            const StrataRegs& sr, uint32_t& a1, uint32_t& a2) {
+  using G = Geo<N, EST, MODEL>;
   constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
   static_assert(SAMPLES_PER_THREAD % G::L == 0, "L must divide the per-thread run");
   uint64_t q = s_begin * (uint64_t)G::U / 4;   // first Philox block of this thread's run
   const uint32_t one = one_bits_reg();
-#if MC_PIPELINE
-  if constexpr (!MASKED) {
-    // software-pipelined: the next step's Philox words are generated while this step's draws are
-    // evaluated (independent instruction streams the scheduler can interleave across pipes)
-    uint32_t w[G::BLOCKS * 4];
-#pragma unroll
-    for (int b = 0; b < G::BLOCKS; ++b) philox_block_rk(q + b, lo1d, hi1d, rk, &w[4 * b]);
-    q += G::BLOCKS;
-#pragma unroll 2
-    for (int st = 0; st < STEPS; ++st) {
-      uint32_t wn[G::BLOCKS * 4];
-#pragma unroll
-      for (int b = 0; b < G::BLOCKS; ++b) philox_block_rk(q + b, lo1d, hi1d, rk, &wn[4 * b]);
-      q += G::BLOCKS;
-#pragma unroll
-      for (int l = 0; l < G::L; ++l) accumulate<EST>(draw_utility<N, EST, false>(&w[l * G::U], one, zc, pr), a1, a2);
-#pragma unroll
-      for (int k = 0; k < G::BLOCKS * 4; ++k) w[k] = wn[k];
-    }
-    if constexpr (EST == 1) a2 = a1;
-    return;
-  }
-#endif
 #pragma unroll 1
   for (int st = 0; st < STEPS; ++st) {
     const uint64_t s0 = s_begin + (uint64_t)st * G::L;
@@ -92,7 +78,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
     q += G::BLOCKS;
 #pragma unroll
     for (int l = 0; l < G::L; ++l) {
-      float u = draw_utility<N, EST, false>(&w[l * G::U], one, zc, pr);
+      float u = draw_utility<N, EST, false, MODEL>(&w[l * G::U], one, zc, pr, nullptr, nullptr, &sr);
       if (MASKED) {
         const uint64_t s = s0 + l;
         u = (s >= B && s < E) ? u : 0.0f;
@@ -110,7 +96,7 @@ constexpr int min_blocks(int n, int est) {
   return n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1);
 }
 
-template <int N, int EST>
+template <int N, int EST, int MODEL>
 __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST)) mc_fused_kernel(
     const float* __restrict__ prob, const float* __restrict__ zc_all, const int32_t* __restrict__ pod, int64_t d0,
     uint64_t B, uint64_t E, uint64_t Balign, int64_t tiles_per_design, int64_t total_tiles, const RoundKeys rk,
@@ -122,8 +108,11 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST)) mc_fused_kernel
   for (int64_t tile = gw; tile < total_tiles; tile += nw) {
     const int64_t d = d0 + tile / tiles_per_design;
     const int64_t chunk = tile % tiles_per_design;
+    const float* rec = prob + (int64_t)__ldg(pod + d) * PROB_STRIDE;
     ProbRegs<N> pr;
-    load_problem<N>(prob + (int64_t)__ldg(pod + d) * PROB_STRIDE, pr);
+    load_problem<N>(rec, pr);
+    StrataRegs sr;
+    if constexpr (MODEL == 1) load_strata(rec, sr);
     float zc[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) zc[i] = __ldg(zc_all + d * N + i);
@@ -132,9 +121,9 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST)) mc_fused_kernel
     const uint64_t s_begin = Balign + (uint64_t)chunk * tile_samples + (uint64_t)lane * SAMPLES_PER_THREAD;
     uint32_t a1 = 0, a2 = 0;
     if (s_begin >= B && s_begin + SAMPLES_PER_THREAD <= E)
-      run_samples<N, EST, false>(s_begin, B, E, lo1d, hi1d, rk, zc, pr, a1, a2);
+      run_samples<N, EST, false, MODEL>(s_begin, B, E, lo1d, hi1d, rk, zc, pr, sr, a1, a2);
     else if (s_begin < E)
-      run_samples<N, EST, true>(s_begin, B, E, lo1d, hi1d, rk, zc, pr, a1, a2);
+      run_samples<N, EST, true, MODEL>(s_begin, B, E, lo1d, hi1d, rk, zc, pr, sr, a1, a2);
     unsigned long long v1 = a1, v2 = a2;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -148,10 +137,10 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST)) mc_fused_kernel
   }
 }
 
-template <int N, int EST>
+template <int N, int EST, int MODEL = 0>
 static cudaError_t launch_fused_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
                                   int64_t* sums) {
-  using G = Geo<N, EST>;
+  using G = Geo<N, EST, MODEL>;
   const int threads = c->block_threads;
   const uint64_t tile = 32ull * SAMPLES_PER_THREAD;   // one warp tile
   const uint64_t Balign = B - (B % G::L);
@@ -162,14 +151,15 @@ static cudaError_t launch_fused_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mc_fused_kernel<N, EST>, threads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mc_fused_kernel<N, EST, MODEL>, threads, 0);
     grid = nsm * (per > 0 ? per : 1);
   }
   const int64_t warps_needed = total, wpb = threads / 32;
   if ((int64_t)grid * wpb > warps_needed) grid = (int)((warps_needed + wpb - 1) / wpb);
   if (grid <= 0) return cudaSuccess;
-  mc_fused_kernel<N, EST><<<grid, threads, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, d0, B, E, Balign, tpd, total,
-                                                    round_keys(c->seed), reinterpret_cast<unsigned long long*>(sums));
+  mc_fused_kernel<N, EST, MODEL><<<grid, threads, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, d0, B, E, Balign, tpd,
+                                                           total, round_keys(c->seed),
+                                                           reinterpret_cast<unsigned long long*>(sums));
   c->launches += 1;
   return cudaGetLastError();
 }
@@ -193,6 +183,11 @@ template <int EST>
 static mc_status launch_fused_est(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
                                   int64_t* sums) {
   cudaError_t e = cudaSuccess;
+  if (c->model == 1) {
+    e = launch_fused_t<2, EST, 1>(c, d0, dcount, B, E, st, sums);
+    if (e != cudaSuccess) return cuda_fail(e, "mc_fused_kernel launch");
+    return MC_OK;
+  }
   MC_DISPATCH_N(launch_fused_t, c, d0, dcount, B, E, st, sums);
   if (e != cudaSuccess) return cuda_fail(e, "mc_fused_kernel launch");
   return MC_OK;
@@ -204,11 +199,15 @@ mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64
                      : launch_fused_est<1>(c, d0, dcount, B, E, st, sums);
 }
 
-int words_per_draw(int n, int est) {
-  // Geo<N,EST>::U without instantiating every N
-  return est == 0 ? 2 * ((n + 1) / 2) + n / 2 : 2 * ((2 * n + 1) / 2);
+int words_per_draw(int n, int est, int model) {
+  // Geo<N,EST,MODEL>::U without instantiating every N
+  const int p = model == 1 ? 5 : n;
+  return est == 0 ? 2 * ((p + 1) / 2) + n / 2 : 2 * ((p + n + 1) / 2);
 }
-int draw_dump_stride(int n, int est) { return (est == 0 ? n : 2 * n) + n + 1; }
+int draw_dump_stride(int n, int est, int model) {
+  const int p = model == 1 ? 5 : n;
+  return (est == 0 ? p : p + n) + n + 1;
+}
 
 // ---------------------------------------------------------------------------------------------
 // Design thresholds (row a1): zc_i = Z_{1-alpha_i} - c_i theta_i in fp64 -> fp32; alpha = 0 -> +inf.
@@ -273,16 +272,18 @@ mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64
 }
 
 // Per-draw dump through the fused kernel's draw_utility (test hook).
-template <int N, int EST>
+template <int N, int EST, int MODEL>
 __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restrict__ zc_all,
                             const int32_t* __restrict__ pod, uint64_t seed, const int64_t* __restrict__ design,
                             const uint64_t* __restrict__ sample, int64_t count, float* __restrict__ out) {
-  using G = Geo<N, EST>;
+  using G = Geo<N, EST, MODEL>;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= count) return;
   const int64_t d = design[i];
   ProbRegs<N> pr;
   load_problem<N>(prob + (int64_t)pod[d] * PROB_STRIDE, pr);
+  StrataRegs sr;
+  if constexpr (MODEL == 1) load_strata(prob + (int64_t)pod[d] * PROB_STRIDE, sr);
   float zc[N];
   for (int k = 0; k < N; ++k) zc[k] = zc_all[d * N + k];
   uint32_t w[G::U];
@@ -290,14 +291,14 @@ __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restr
   for (int k = 0; k < G::U; ++k) w[k] = philox_word(seed, (uint32_t)d, base + k);
   float bsc[N];
   for (int k = 0; k < N; ++k) bsc[k] = prob[(int64_t)pod[d] * PROB_STRIDE + OFF_BSC + k];
-  draw_utility<N, EST, true>(w, 0x3F800000u, zc, pr, out + i * G::DUMP, bsc);
+  draw_utility<N, EST, true, MODEL>(w, 0x3F800000u, zc, pr, out + i * G::DUMP, bsc, &sr);
 }
 
-template <int N, int EST>
+template <int N, int EST, int MODEL = 0>
 static cudaError_t launch_dump_t(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
                                  cudaStream_t st) {
-  k_draw_dump<N, EST><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, c->seed, design,
-                                                                      sample, count, out);
+  k_draw_dump<N, EST, MODEL><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, c->seed,
+                                                                             design, sample, count, out);
   return cudaGetLastError();
 }
 
@@ -305,6 +306,11 @@ template <int EST>
 static mc_status launch_dump_est(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
                                  cudaStream_t st) {
   cudaError_t e = cudaSuccess;
+  if (c->model == 1) {
+    e = launch_dump_t<2, EST, 1>(c, design, sample, count, out, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_draw_dump launch");
+    return MC_OK;
+  }
   MC_DISPATCH_N(launch_dump_t, c, design, sample, count, out, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_draw_dump launch");
   return MC_OK;

@@ -31,7 +31,8 @@ class mc_problem(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("has_prior_chol", ctypes.c_int32), ("i3", ctypes.c_double),
                 ("alpha0", ctypes.c_double), ("r", ctypes.c_double * MC_MAX_N),
                 ("theta", ctypes.c_double * MC_MAX_N), ("sigma", ctypes.c_double * MC_MAX_N),
-                ("prior_chol", ctypes.c_double * (MC_MAX_N * MC_MAX_N))]
+                ("prior_chol", ctypes.c_double * (MC_MAX_N * MC_MAX_N)), ("model", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("strata", ctypes.c_double * 10)]
 
 
 _lib = None
@@ -57,6 +58,7 @@ def lib() -> ctypes.CDLL:
         L.mc_information_units.argtypes = [d, d, d]; L.mc_information_units.restype = d
         L.mc_threshold.argtypes = [d]; L.mc_threshold.restype = d
         L.mc_problem_formula10.argtypes = [i32, P(d), P(d), d, d, P(mc_problem)]; L.mc_problem_formula10.restype = i32
+        L.mc_problem_strata.argtypes = [d, d, d, P(d), P(mc_problem)]; L.mc_problem_strata.restype = i32
         L.mc_fwer.argtypes = [P(mc_problem), P(d), i64, P(d), i32]; L.mc_fwer.restype = i32
         L.mc_candidates.argtypes = [P(mc_problem), i32, i32, i64, u64, P(d), P(i32), i64, P(i64), i32]
         L.mc_candidates.restype = i32
@@ -81,7 +83,7 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_fwer", "mc_candidates",
+EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer", "mc_candidates",
             "mc_design_init", "mc_design_upload", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
             "mc_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
@@ -125,6 +127,14 @@ def problem_formula10(r, delta0, i3: float, alpha0: float = 0.025) -> mc_problem
     d0 = np.ascontiguousarray(delta0, dtype=np.float64)
     p = mc_problem()
     _check(lib().mc_problem_formula10(len(r), _dp(r), _dp(d0), float(i3), float(alpha0), ctypes.byref(p)))
+    return p
+
+
+def problem_strata(r2: float, i3: float, strata, alpha0: float = 0.025) -> mc_problem:
+    """C4 strata prior (n = 2)."""
+    sp = np.ascontiguousarray(strata, dtype=np.float64)
+    p = mc_problem()
+    _check(lib().mc_problem_strata(float(r2), float(i3), float(alpha0), _dp(sp), ctypes.byref(p)))
     return p
 
 

@@ -68,3 +68,16 @@ def c5_problem(n: int):
 
 # draws per design (BASELINE.json configs)
 DRAWS = {"C1": 10_000, "C2": 1_000_000, "C3": 1_000_000_000, "C5": 1_000_000}
+
+
+# C4: synthetic 5-D strata prior (not in the paper), n = 2, dense 256 x 256 design grid
+# r2 = (i + 1/2)/256 x alpha_1 = (j + 1/2) alpha0/256 (alpha_2 solved), I3 = 211.
+# (mean, sd) of: logit prevalence, effect+, effect-, log variance, logit dropout.
+import math as _math
+
+C4_STRATA = (_math.log(0.35 / 0.65), 0.4, 0.6, 0.15, 0.05, 0.10, 0.0, 0.2, _math.log(0.1 / 0.9), 0.5)
+C4_GRID = 256
+
+
+def c4_r2_values(m: int = C4_GRID):
+    return [(i + 0.5) / m for i in range(m)]

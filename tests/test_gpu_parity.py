@@ -292,3 +292,45 @@ def test_dimension_sweep_parity(O, mc, torch, n, est):
             assert abs(rec[i, -1] - o["u"]) <= 5e-5
         else:
             assert rec[i, -1] == o["u"] or np.min(np.abs(o["xnull"] - o["b"])) < 1e-4
+
+
+@pytest.mark.parametrize("est", [0, 1])
+def test_c4_strata_prior_parity(O, mc, torch, est):
+    """C4 (5-D strata prior, n = 2, BASELINE configs[3]): a slice of the 256 x 256 (r2 x alpha_1) grid."""
+    sp = np.array(W.C4_STRATA)
+    r2s = [W.c4_r2_values()[i] for i in (10, 77, 150, 240)]
+    probs, alpha, pod = [], [], []
+    for k, r2 in enumerate(r2s):
+        probs.append(mc.problem_strata(r2, 211.0, sp))
+        for j in (3, 128, 250):
+            a1 = (j + 0.5) * 0.025 / 256
+            alpha.append([a1, O.solve_alpha_n([1.0, r2], 0.025, [a1], 1e-13)])
+            pod.append(k)
+    alpha = np.array(alpha)
+    dsg = mc.Design(probs, alpha, np.array(pod, dtype=np.int32), seed=SEED, estimator=est)
+    assert dsg.words_per_draw == (7 if est == 0 else 8)
+    N = 40_000
+    sums = dsg.new_sums()
+    dsg.evaluate(sums, 0, N)
+    got = dsg.finalize(sums, N)[0].cpu().numpy()
+    flips = 0
+    for d in range(len(alpha)):
+        r2 = r2s[pod[d]]
+        ref_s = O.design_sums_strata(r2, 211.0, sp, alpha[d], est, SEED, d, 0, N)
+        if est == 0:
+            ref = O.finalize(ref_s, N)[0][0]
+            assert abs(got[d] - ref) <= REL * ref, (d, got[d], ref)
+        else:
+            flips += abs(int(sums[d, 0].item()) - int(ref_s[0])) // 2**23
+    assert flips <= 2
+    D = torch.tensor(list(range(len(alpha))) * 4).cuda()
+    S = torch.arange(4 * len(alpha)).cuda() * 104729 + 3
+    rec = dsg.draw_dump(D, S).cpu().numpy().astype(np.float64)
+    for i in range(len(D)):
+        d = int(D[i])
+        o = O.draw_strata(r2s[pod[d]], 211.0, sp, alpha[d], est, SEED, d, int(S[i]))
+        assert np.allclose(rec[i, :5], o["eps"], atol=5e-6 * (1 + np.abs(o["eps"]).max()) + 1e-3 * (np.abs(o["eps"]).min() < 1e-2))
+        nn = 5 if est == 0 else 7
+        assert np.allclose(rec[i, nn:nn + 2], o["b"], atol=2e-4 * (1 + np.abs(o["b"]).max()))
+        if est == 0:
+            assert abs(rec[i, -1] - o["u"]) <= 1e-4

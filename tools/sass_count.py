@@ -24,10 +24,10 @@ def draws_per_iter(n: int, est: int) -> int:
     return 4 // math.gcd(U, 4)
 
 
-def sass(n: int, est: int, lib: str = None):
+def sass(n: int, est: int, lib: str = None, model: int = 0):
     out = subprocess.run(["cuobjdump", "-sass", lib or LIB], capture_output=True, text=True).stdout
     # select the function body of mc_fused_kernel<n, est>
-    tag = f"_ZN3mci15mc_fused_kernelILi{n}ELi{est}EEEv"
+    tag = f"_ZN3mci15mc_fused_kernelILi{n}ELi{est}ELi{model}EEEv"
     lines, on = [], False
     for line in out.splitlines():
         if "Function :" in line:
