@@ -170,6 +170,26 @@ mc_status mc_smooth_plan(mc_ctx* ctx, const uint8_t* fit_mask_host, void* cuda_s
 mc_status mc_smooth(mc_ctx* ctx, const double* values_dev, double lambda, double* smoothed_dev,
                     double* lambda_used_dev, void* cuda_stream);
 
+/* ---- NEXT f1: the continuous optimum on the smoothed surface ------------------ */
+
+/* Fits (and caches in the ctx) every problem's TPS coefficients through values_dev[D] with lambda
+ * (< 0: GCV, as mc_smooth): w on the GPU from the plan, beta on the host.  Synchronises. */
+mc_status mc_tps_fit(mc_ctx* ctx, const double* values_dev, double lambda, void* cuda_stream);
+
+/* Evaluates the cached TPS surface of `problem` at q points x_host[q*d] (x = alpha_{1..d}/alpha0,
+ * d = n-1): f_host[q] and, if non-NULL, grad_host[q*d].  Host only. */
+mc_status mc_tps_eval(const mc_ctx* ctx, int32_t problem, const double* x_host, int64_t q, double* f_host,
+                      double* grad_host);
+
+/* Per problem: maximises the TPS surface (mc_tps_fit with lambda) by box-constrained limited-memory
+ * quasi-Newton (projected L-BFGS, memory 10) started from the fitted design with the largest P~ over
+ * the box spanned by the fitted designs; re-solves alpha_n from Formula 2 (GPU, fp64).  Writes
+ * alpha_out_host[n_probs*n], value_out_host[n_probs] (P~ at the optimum) and status_out_host[n_probs]:
+ * 0 = ok, 1 = the optimum's alpha_n is infeasible (alpha_n = NaN), 2 = no surface (n = 1 or too few
+ * designs: the best evaluated design is returned).  Synchronises. */
+mc_status mc_refine(mc_ctx* ctx, const double* values_dev, double lambda, double* alpha_out_host,
+                    double* value_out_host, int32_t* status_out_host, void* cuda_stream);
+
 /* ---- a10: argmax --------------------------------------------------------------- */
 
 /* Per problem: the design with the largest value (lowest index on ties; NaN never wins) ->

@@ -470,3 +470,40 @@ def assurance_strata_quadrature(r2: float, i3: float, sp, alpha, n_gh: int = 8, 
                         b = strata_b(r2, i3, sp, z, e)
                         total += w1[i1] * wh[i2] * wh[i3_] * wh[i4] * wh[i5] * (1.0 - mvn_orthant(r, b))
     return float(total)
+
+
+# --------------------------------------------------------------------------------------
+# NEXT f1: continuous optimum on the TPS surface (P:123 L-BFGS-B, P:219 start at the best site)
+
+def tps_eval(sites, w, beta, x):
+    """f(x) = beta_0 + beta_{1..d} x + sum_i w_i phi(|x - x_i|) and its gradient."""
+    sites = np.atleast_2d(np.asarray(sites, dtype=np.float64))
+    d = sites.shape[1]
+    x = np.asarray(x, dtype=np.float64)
+    diff = x[None, :] - sites
+    r = np.sqrt((diff ** 2).sum(1))
+    f = beta[0] + beta[1:] @ x + w @ tps_phi(r, d)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        if d == 1:
+            dphi_r = 3 * r
+        elif d == 2:
+            dphi_r = np.where(r > 0, 2 * np.log(np.where(r > 0, r, 1.0)) + 1.0, 0.0)
+        else:
+            dphi_r = np.where(r > 0, -1.0 / np.where(r > 0, r, 1.0), 0.0)
+    grad = beta[1:] + (w * dphi_r) @ diff
+    return float(f), grad
+
+
+def refine(sites, y, lam: float = -1.0):
+    """Maximise the fitted TPS by scipy's L-BFGS-B (a library routine) from the fitted site with the
+    largest value over the sites' bounding box.  Returns (x*, f*, lambda)."""
+    from scipy.optimize import minimize
+    sites = np.atleast_2d(np.asarray(sites, dtype=np.float64))
+    if lam < 0:
+        _, lam = tps_smooth(sites, y, -1.0)
+    fitted, w, beta = tps_fit(sites, y, lam)
+    x0 = sites[int(np.argmax([tps_eval(sites, w, beta, s)[0] for s in sites]))]
+    bounds = list(zip(sites.min(0), sites.max(0)))
+    res = minimize(lambda x: tuple(-v for v in tps_eval(sites, w, beta, x)), x0, jac=True, method="L-BFGS-B",
+                   bounds=bounds, options={"ftol": 1e-15, "gtol": 1e-12, "maxiter": 500, "maxcor": 10})
+    return res.x, -float(res.fun), lam

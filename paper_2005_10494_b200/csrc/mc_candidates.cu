@@ -167,23 +167,11 @@ __global__ void k_fwer(ProbChain pc, const double* __restrict__ alpha, int64_t c
   out[i] = fwer_dev<CHAIN>(a, pc.ch);
 }
 
-// One thread per (problem, grid point): feasibility and alpha_n by the Illinois method on
-// f(a) = FWER(alpha_1..alpha_{n-1}, a) - alpha0, increasing in a.
+// Feasibility and alpha_n for partial alpha a[0..n-2] by the Illinois method on
+// f(x) = FWER(alpha_1..alpha_{n-1}, x) - alpha0, increasing in x.  Writes a[n-1].
 template <bool CHAIN>
-__global__ void k_alpha_grid(const ProbChain* __restrict__ pcs, int32_t n_probs, int32_t m, int64_t G,
-                             double* __restrict__ A, uint8_t* __restrict__ valid) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)n_probs * G) return;
-  const int k = (int)(t / G);
-  const int64_t g = t % G;
-  const ProbChain pc = pcs[k];
+__device__ uint8_t solve_alpha_n_dev(const ProbChain& pc, double* a) {
   const int n = pc.ch.n;
-  double a[MC_MAX_N];
-  int64_t rem = g;
-  for (int i = n - 2; i >= 0; --i) {
-    a[i] = ((double)(rem % m) + 0.5) * pc.alpha0 / m;
-    rem /= m;
-  }
   double an = pc.alpha0;
   uint8_t ok = 1;
   if (n > 1) {
@@ -215,9 +203,43 @@ __global__ void k_alpha_grid(const ProbChain* __restrict__ pcs, int32_t n_probs,
       }
     }
   }
-  for (int i = 0; i + 1 < n; ++i) A[t * n + i] = a[i];
-  A[t * n + n - 1] = an;
+  a[n - 1] = an;
+  return ok;
+}
+
+// One thread per (problem, grid point) of the half-offset m^(n-1) grid.
+template <bool CHAIN>
+__global__ void k_alpha_grid(const ProbChain* __restrict__ pcs, int32_t n_probs, int32_t m, int64_t G,
+                             double* __restrict__ A, uint8_t* __restrict__ valid) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n_probs * G) return;
+  const int k = (int)(t / G);
+  const int64_t g = t % G;
+  const ProbChain pc = pcs[k];
+  const int n = pc.ch.n;
+  double a[MC_MAX_N];
+  int64_t rem = g;
+  for (int i = n - 2; i >= 0; --i) {
+    a[i] = ((double)(rem % m) + 0.5) * pc.alpha0 / m;
+    rem /= m;
+  }
+  const uint8_t ok = solve_alpha_n_dev<CHAIN>(pc, a);
+  for (int i = 0; i < n; ++i) A[t * n + i] = a[i];
   valid[t] = ok;
+}
+
+// One thread per explicit partial point (problem index, alpha_1..alpha_{n-1}): alpha_n in place.
+template <bool CHAIN>
+__global__ void k_alpha_points(const ProbChain* __restrict__ pcs, const int32_t* __restrict__ prob, int64_t count,
+                               double* __restrict__ A, uint8_t* __restrict__ valid) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const ProbChain pc = pcs[prob[t]];
+  const int n = pc.ch.n;
+  double a[MC_MAX_N];
+  for (int i = 0; i < n; ++i) a[i] = A[t * n + i];
+  valid[t] = solve_alpha_n_dev<CHAIN>(pc, a);
+  A[t * n + n - 1] = a[n - 1];
 }
 
 static ProbChain make_chain(const mc_problem& p) {
@@ -266,6 +288,46 @@ mc_status alpha_grid_solve(const mc_problem* probs, int32_t n_probs, int32_t m, 
     }
   }
   cudaFree(d_pcs);
+  cudaFree(d_A);
+  cudaFree(d_v);
+  return s;
+}
+
+mc_status alpha_points_solve(const mc_problem* probs, int32_t n_probs, const int32_t* prob, int64_t count, int device,
+                             double* A, uint8_t* valid) {
+  if (count <= 0) return MC_OK;
+  MC_CUDA(cudaSetDevice(device));
+  MC_CUDA(upload_gl());
+  const int n = probs[0].n;
+  std::vector<ProbChain> pcs(n_probs);
+  for (int k = 0; k < n_probs; ++k) pcs[k] = make_chain(probs[k]);
+  ProbChain* d_pcs = nullptr;
+  int32_t* d_prob = nullptr;
+  double* d_A = nullptr;
+  uint8_t* d_v = nullptr;
+  mc_status s = MC_OK;
+  cudaError_t e;
+  if ((e = cudaMalloc(&d_pcs, sizeof(ProbChain) * n_probs)) != cudaSuccess ||
+      (e = cudaMalloc(&d_prob, sizeof(int32_t) * count)) != cudaSuccess ||
+      (e = cudaMalloc(&d_A, sizeof(double) * count * n)) != cudaSuccess ||
+      (e = cudaMalloc(&d_v, count)) != cudaSuccess) {
+    s = cuda_fail(e, "alpha_points_solve alloc");
+  } else if ((e = cudaMemcpy(d_pcs, pcs.data(), sizeof(ProbChain) * n_probs, cudaMemcpyHostToDevice)) != cudaSuccess ||
+             (e = cudaMemcpy(d_prob, prob, sizeof(int32_t) * count, cudaMemcpyHostToDevice)) != cudaSuccess ||
+             (e = cudaMemcpy(d_A, A, sizeof(double) * count * n, cudaMemcpyHostToDevice)) != cudaSuccess) {
+    s = cuda_fail(e, "alpha_points_solve upload");
+  } else {
+    const int threads = n >= 4 ? 32 : 128;
+    const unsigned blocks = (unsigned)((count + threads - 1) / threads);
+    if (n >= 4) k_alpha_points<true><<<blocks, threads>>>(d_pcs, d_prob, count, d_A, d_v);
+    else k_alpha_points<false><<<blocks, threads>>>(d_pcs, d_prob, count, d_A, d_v);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess ||
+        (e = cudaMemcpy(A, d_A, sizeof(double) * count * n, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+        (e = cudaMemcpy(valid, d_v, count, cudaMemcpyDeviceToHost)) != cudaSuccess)
+      s = cuda_fail(e, "k_alpha_points");
+  }
+  cudaFree(d_pcs);
+  cudaFree(d_prob);
   cudaFree(d_A);
   cudaFree(d_v);
   return s;

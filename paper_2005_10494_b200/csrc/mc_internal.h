@@ -80,6 +80,10 @@ struct mc_ctx {
   std::vector<mci::TpsPlan> plans;
   double* d_tps_scratch = nullptr;       // per-problem scratch for smoothing
   size_t tps_scratch_elems = 0;
+  int n_plans = 0;
+  // TPS coefficients of the last mc_refine (host): per problem sites, w, beta
+  std::vector<std::vector<double>> tps_x, tps_w, tps_beta;
+  std::vector<double> tps_lambda;
 };
 
 // launchers implemented in the .cu files
@@ -97,8 +101,11 @@ mc_status launch_zc(mc_ctx* c, cudaStream_t st);
 mc_status launch_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, cudaStream_t st);
 mc_status alpha_grid_solve(const mc_problem* probs, int32_t n_probs, int32_t m, int device,
                            std::vector<double>& alpha, std::vector<uint8_t>& valid);
+mc_status alpha_points_solve(const mc_problem* probs, int32_t n_probs, const int32_t* prob, int64_t count, int device,
+                             double* A, uint8_t* valid);
 mc_status fwer_eval(const mc_problem* p, const double* alpha, int64_t count, double* out, int device);
 mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st);
+mc_status tps_coefficients(mc_ctx* c, const double* values, double lambda, cudaStream_t st);
 mc_status smooth_apply(mc_ctx* c, const double* values, double lambda, double* out, double* lam_used,
                        cudaStream_t st);
 }  // namespace mci

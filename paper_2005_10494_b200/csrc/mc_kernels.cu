@@ -92,12 +92,12 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
 // Work unit = one WARP tile: (design, 32 x SAMPLES_PER_THREAD consecutive samples).  Warps are
 // independent (no block barrier): each reduces its tile with 64-bit shuffles and lane 0 issues one
 // 64-bit atomicAdd pair.  Warp tiles are strided over the persistent grid's warps.
-constexpr int min_blocks(int n, int est) {
-  return n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1);
+constexpr int min_blocks(int n, int est, int model) {
+  return model == 1 ? 3 : (n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1));
 }
 
 template <int N, int EST, int MODEL>
-__global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST)) mc_fused_kernel(
+__global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused_kernel(
     const float* __restrict__ prob, const float* __restrict__ zc_all, const int32_t* __restrict__ pod, int64_t d0,
     uint64_t B, uint64_t E, uint64_t Balign, int64_t tiles_per_design, int64_t total_tiles, const RoundKeys rk,
     unsigned long long* __restrict__ sums) {

@@ -107,6 +107,9 @@ struct PlanDev {
   int64_t N;      // fitted sites
   int64_t k;      // N - (d+1) eigen-columns
   int64_t off;    // offset into the c / y scratch
+  int32_t prob;   // problem index
+  int32_t d;      // TPS dimension
+  double alpha0;  // coordinate scale x = alpha / alpha0
 };
 
 __global__ void k_gather(const PlanDev* __restrict__ pl, const double* __restrict__ values, double* __restrict__ y) {
@@ -129,9 +132,11 @@ __global__ void k_et_y(const PlanDev* __restrict__ pl, const double* __restrict_
   if (lane == 0) c[p.off + j] = acc;
 }
 
-// GCV over the log grid (or the fixed lambda), then c_j <- t_j c_j.  One block per problem.
+// GCV over the log grid (or the fixed lambda), then c_j <- t_j c_j (mode 0: smoothing,
+// t_j = N lambda / (Lambda_j + N lambda)) or c_j <- c_j / (Lambda_j + N lambda) (mode 1: the TPS kernel
+// weights w = E (c ./ (Lambda + N lambda))).  One block per problem; lambda written to lam_used[prob].
 __global__ void k_gcv(const PlanDev* __restrict__ pl, double lambda_fixed, double* __restrict__ c,
-                      double* __restrict__ lam_used) {
+                      double* __restrict__ lam_used, int mode) {
   __shared__ double s_rss[32], s_tr[32];
   __shared__ double s_best;
   const PlanDev p = pl[blockIdx.x];
@@ -167,9 +172,41 @@ __global__ void k_gcv(const PlanDev* __restrict__ pl, double lambda_fixed, doubl
     __syncthreads();
     lam = s_best;
   }
-  if (threadIdx.x == 0 && lam_used) lam_used[blockIdx.x] = lam;
+  if (threadIdx.x == 0 && lam_used) lam_used[p.prob] = lam;
   const double nl = Nd * lam;
-  for (int64_t j = threadIdx.x; j < p.k; j += blockDim.x) c[p.off + j] *= nl / (p.lam[j] + nl);
+  for (int64_t j = threadIdx.x; j < p.k; j += blockDim.x)
+    c[p.off + j] *= (mode == 0 ? nl : 1.0) / (p.lam[j] + nl);
+}
+
+// w_i = sum_j E_ij g_j  (thread per row)
+__global__ void k_e_w(const PlanDev* __restrict__ pl, const double* __restrict__ g, double* __restrict__ w) {
+  const PlanDev p = pl[blockIdx.y];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  const double* gg = g + p.off;
+  double acc = 0.0;
+  for (int64_t j = 0; j < p.k; ++j) acc += p.E[i + j * p.N] * gg[j];
+  w[p.off + i] = acc;
+}
+
+// (K w)_i = sum_j phi(|x_i - x_j|) w_j with x = alpha_{1..d} / alpha0 (thread per row)
+__global__ void k_tps_kw(const PlanDev* __restrict__ pl, const double* __restrict__ alpha, int n,
+                         const double* __restrict__ w, double* __restrict__ kw) {
+  const PlanDev p = pl[blockIdx.y];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  const double* xi = alpha + p.fit_idx[i] * n;
+  double acc = 0.0;
+  for (int64_t j = 0; j < p.N; ++j) {
+    const double* xj = alpha + p.fit_idx[j] * n;
+    double r2 = 0.0;
+    for (int k = 0; k < p.d; ++k) {
+      const double t = (xi[k] - xj[k]) / p.alpha0;
+      r2 += t * t;
+    }
+    acc += tps_phi(sqrt(r2), p.d) * w[p.off + j];
+  }
+  kw[p.off + i] = acc;
 }
 
 // out[fit_idx[i]] = y_i - sum_j E_ij c_j   (thread per row; the j-loop reads E coalesced)
@@ -366,15 +403,19 @@ mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
   if (tot > 0) {
     // y [tot], c [tot], PlanDev table
     const size_t bytes = sizeof(double) * 2 * tot + sizeof(PlanDev) * c->n_probs + 64;
+    c->n_plans = 0;
     MC_CUDA(cudaMalloc(&c->d_tps_scratch, bytes));
     c->tps_scratch_elems = (size_t)tot;
     std::vector<PlanDev> pd;
     int64_t off = 0;
-    for (auto& pl : c->plans) {
+    for (int k = 0; k < c->n_probs; ++k) {
+      const auto& pl = c->plans[k];
       if (pl.passthrough) continue;
-      pd.push_back(PlanDev{pl.d_E, pl.d_lam, pl.d_fit_idx, pl.nfit, pl.nfit - pl.d - 1, off});
+      pd.push_back(PlanDev{pl.d_E, pl.d_lam, pl.d_fit_idx, pl.nfit, pl.nfit - pl.d - 1, off, k, pl.d,
+                           c->probs[k].alpha0});
       off += pl.nfit;
     }
+    c->n_plans = (int)pd.size();
     MC_CUDA(cudaMemcpy(reinterpret_cast<char*>(c->d_tps_scratch) + sizeof(double) * 2 * tot, pd.data(),
                        sizeof(PlanDev) * pd.size(), cudaMemcpyHostToDevice));
   }
@@ -402,22 +443,114 @@ mc_status smooth_apply(mc_ctx* c, const double* values, double lambda, double* o
   double* y = c->d_tps_scratch;
   double* cc = y + tot;
   const PlanDev* pd = reinterpret_cast<const PlanDev*>(reinterpret_cast<char*>(c->d_tps_scratch) + sizeof(double) * 2 * tot);
-  double* lam_tmp = nullptr;
-  if (lam_used) MC_CUDA(cudaMallocAsync(&lam_tmp, sizeof(double) * np, st));
   k_gather<<<dim3(8, np), 256, 0, st>>>(pd, values, y);
   k_et_y<<<dim3((unsigned)((kmax + 7) / 8), np), 256, 0, st>>>(pd, y, cc);
-  k_gcv<<<np, 256, 0, st>>>(pd, lambda, cc, lam_tmp);
+  k_gcv<<<np, 256, 0, st>>>(pd, lambda, cc, lam_used, 0);
   k_e_c<<<dim3((unsigned)((Nmax + 127) / 128), np), 128, 0, st>>>(pd, y, cc, out);
   c->launches += 4;
   MC_CUDA(cudaGetLastError());
-  if (lam_used) {
-    // scatter per-plan lambdas to their problem slots
-    std::vector<int> slot;
-    for (int k = 0; k < c->n_probs; ++k)
-      if (!c->plans[k].passthrough) slot.push_back(k);
-    for (int i = 0; i < np; ++i)
-      MC_CUDA(cudaMemcpyAsync(lam_used + slot[i], lam_tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, st));
-    MC_CUDA(cudaFreeAsync(lam_tmp, st));
+  return MC_OK;
+}
+
+}  // namespace mci
+
+namespace mci {
+
+// TPS coefficients (w, beta) of every problem's surface through values (row a9 -> NEXT f1): on the GPU
+// c = E^T y, lambda by GCV (or fixed), g = c ./ (Lambda + N lambda), w = E g, K w; on the host
+// beta = argmin |T beta - (y - N lambda w - K w)| (the fitted values minus the kernel part; exact since
+// (K + N lambda I) w + T beta = y).  Cached in the ctx (tps_x, tps_w, tps_beta, tps_lambda).
+mc_status tps_coefficients(mc_ctx* c, const double* values, double lambda, cudaStream_t st) {
+  if (!c->plan_built) {
+    mc_status s = smooth_plan(c, nullptr, st);
+    if (s != MC_OK) return s;
+  }
+  c->tps_x.assign(c->n_probs, {});
+  c->tps_w.assign(c->n_probs, {});
+  c->tps_beta.assign(c->n_probs, {});
+  c->tps_lambda.assign(c->n_probs, 0.0);
+  const int np = c->n_plans;
+  if (np == 0) return MC_OK;
+  int64_t Nmax = 0, kmax = 0;
+  for (auto& pl : c->plans)
+    if (!pl.passthrough) {
+      Nmax = std::max(Nmax, pl.nfit);
+      kmax = std::max(kmax, pl.nfit - pl.d - 1);
+    }
+  const int64_t tot = (int64_t)c->tps_scratch_elems;
+  double* y = c->d_tps_scratch;
+  double* cc = y + tot;
+  const PlanDev* pd = reinterpret_cast<const PlanDev*>(reinterpret_cast<char*>(c->d_tps_scratch) + sizeof(double) * 2 * tot);
+  double *w = nullptr, *kw = nullptr, *lam = nullptr;
+  MC_CUDA(cudaMallocAsync(&w, sizeof(double) * tot, st));
+  MC_CUDA(cudaMallocAsync(&kw, sizeof(double) * tot, st));
+  MC_CUDA(cudaMallocAsync(&lam, sizeof(double) * c->n_probs, st));
+  k_gather<<<dim3(8, np), 256, 0, st>>>(pd, values, y);
+  k_et_y<<<dim3((unsigned)((kmax + 7) / 8), np), 256, 0, st>>>(pd, y, cc);
+  k_gcv<<<np, 256, 0, st>>>(pd, lambda, cc, lam, 1);
+  k_e_w<<<dim3((unsigned)((Nmax + 127) / 128), np), 128, 0, st>>>(pd, cc, w);
+  k_tps_kw<<<dim3((unsigned)((Nmax + 127) / 128), np), 128, 0, st>>>(pd, c->d_alpha, c->n, w, kw);
+  c->launches += 5;
+  MC_CUDA(cudaGetLastError());
+  std::vector<double> hy(tot), hw(tot), hkw(tot), hl(c->n_probs);
+  MC_CUDA(cudaMemcpyAsync(hy.data(), y, sizeof(double) * tot, cudaMemcpyDeviceToHost, st));
+  MC_CUDA(cudaMemcpyAsync(hw.data(), w, sizeof(double) * tot, cudaMemcpyDeviceToHost, st));
+  MC_CUDA(cudaMemcpyAsync(hkw.data(), kw, sizeof(double) * tot, cudaMemcpyDeviceToHost, st));
+  MC_CUDA(cudaMemcpyAsync(hl.data(), lam, sizeof(double) * c->n_probs, cudaMemcpyDeviceToHost, st));
+  MC_CUDA(cudaStreamSynchronize(st));
+  cudaFree(w);
+  cudaFree(kw);
+  cudaFree(lam);
+  int64_t off = 0;
+  const int n = c->n;
+  for (int k = 0; k < c->n_probs; ++k) {
+    const TpsPlan& pl = c->plans[k];
+    if (pl.passthrough) continue;
+    const int64_t N = pl.nfit;
+    const int d = pl.d;
+    const double a0 = c->probs[k].alpha0;
+    std::vector<int64_t> fit(N);
+    MC_CUDA(cudaMemcpy(fit.data(), pl.d_fit_idx, sizeof(int64_t) * N, cudaMemcpyDeviceToHost));
+    std::vector<double>& X = c->tps_x[k];
+    X.resize((size_t)N * d);
+    for (int64_t i = 0; i < N; ++i)
+      for (int j = 0; j < d; ++j) X[i * d + j] = c->alpha[fit[i] * n + j] / a0;
+    c->tps_w[k].assign(hw.begin() + off, hw.begin() + off + N);
+    c->tps_lambda[k] = hl[k];
+    // normal equations T^T T beta = T^T r, r = y - N lambda w - K w
+    const int m = d + 1;
+    double A[4][4] = {{0}}, b[4] = {0};
+    for (int64_t i = 0; i < N; ++i) {
+      double t[4] = {1.0, 0, 0, 0};
+      for (int j = 0; j < d; ++j) t[j + 1] = X[i * d + j];
+      const double r = hy[off + i] - (double)N * hl[k] * hw[off + i] - hkw[off + i];
+      for (int a = 0; a < m; ++a) {
+        b[a] += t[a] * r;
+        for (int bb = 0; bb < m; ++bb) A[a][bb] += t[a] * t[bb];
+      }
+    }
+    // Gaussian elimination with partial pivoting on the (d+1) x (d+1) system
+    for (int col = 0; col < m; ++col) {
+      int piv = col;
+      for (int r = col + 1; r < m; ++r)
+        if (std::fabs(A[r][col]) > std::fabs(A[piv][col])) piv = r;
+      if (std::fabs(A[piv][col]) < 1e-300) { set_error("tps_coefficients: rank-deficient sites"); return MC_ERR_NUMERIC; }
+      for (int j = 0; j < m; ++j) std::swap(A[col][j], A[piv][j]);
+      std::swap(b[col], b[piv]);
+      for (int r = col + 1; r < m; ++r) {
+        const double f = A[r][col] / A[col][col];
+        for (int j = col; j < m; ++j) A[r][j] -= f * A[col][j];
+        b[r] -= f * b[col];
+      }
+    }
+    std::vector<double> beta(m);
+    for (int r = m - 1; r >= 0; --r) {
+      double acc = b[r];
+      for (int j = r + 1; j < m; ++j) acc -= A[r][j] * beta[j];
+      beta[r] = acc / A[r][r];
+    }
+    c->tps_beta[k] = beta;
+    off += N;
   }
   return MC_OK;
 }

@@ -71,6 +71,9 @@ def lib() -> ctypes.CDLL:
         L.mc_finalize.argtypes = [vp, vp, u64, vp, vp, vp]; L.mc_finalize.restype = i32
         L.mc_smooth_plan.argtypes = [vp, vp, vp]; L.mc_smooth_plan.restype = i32
         L.mc_smooth.argtypes = [vp, vp, d, vp, vp, vp]; L.mc_smooth.restype = i32
+        L.mc_tps_fit.argtypes = [vp, vp, d, vp]; L.mc_tps_fit.restype = i32
+        L.mc_tps_eval.argtypes = [vp, i32, P(d), i64, P(d), P(d)]; L.mc_tps_eval.restype = i32
+        L.mc_refine.argtypes = [vp, vp, d, P(d), P(d), P(i32), vp]; L.mc_refine.restype = i32
         L.mc_argmax.argtypes = [vp, vp, vp, vp, P(i64), P(d), vp]; L.mc_argmax.restype = i32
         L.mc_num_designs.argtypes = [vp]; L.mc_num_designs.restype = i64
         L.mc_num_problems.argtypes = [vp]; L.mc_num_problems.restype = i32
@@ -85,7 +88,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer", "mc_candidates",
             "mc_design_init", "mc_design_upload", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
-            "mc_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
+            "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
 
 
@@ -301,6 +304,25 @@ class Design:
         _check(lib().mc_smooth(self._ctx, values.data_ptr(), float(lam), out.data_ptr(), lam_used.data_ptr(),
                                _stream(stream)))
         return out, lam_used
+
+    def tps_fit(self, values, lam: float = -1.0, stream=None):
+        _check(lib().mc_tps_fit(self._ctx, values.data_ptr(), float(lam), _stream(stream)))
+
+    def tps_eval(self, problem: int, x):
+        x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+        f = np.zeros(x.shape[0])
+        g = np.zeros_like(x)
+        _check(lib().mc_tps_eval(self._ctx, problem, _dp(x), x.shape[0], _dp(f), _dp(g)))
+        return f, g
+
+    def refine(self, values, lam: float = -1.0, stream=None):
+        """NEXT f1: per-problem continuous optimum on the TPS surface (alpha*, P~*, status)."""
+        A = np.zeros((self.n_probs, self.n))
+        v = np.zeros(self.n_probs)
+        st = np.zeros(self.n_probs, dtype=np.int32)
+        _check(lib().mc_refine(self._ctx, values.data_ptr(), float(lam), _dp(A), _dp(v),
+                               st.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _stream(stream)))
+        return A, v, st
 
     def argmax(self, values, with_host: bool = True, stream=None):
         """Row a10: per-problem argmax (device) and, if with_host, the overall (index, value)."""

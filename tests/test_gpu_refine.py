@@ -1,0 +1,76 @@
+"""NEXT f1 on the GPU path: TPS coefficients, surface evaluation and the L-BFGS-B continuous optimum
+against the oracle (scipy L-BFGS-B on the oracle's TPS)."""
+import numpy as np
+import pytest
+
+from paper_2005_10494_b200 import workloads as W
+from tests.helpers import lib_problem, oracle_problem, slice_designs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def mc(torch):
+    from paper_2005_10494_b200 import build, mc as m
+    build.build()
+    return m
+
+
+def _surface(O, m, seed, noise):
+    spec, alpha = slice_designs(O, m=m, count=None)
+    x = alpha[:, :2] / spec.alpha0
+    f = 0.95 + 0.02 * np.exp(-((x[:, 0] - 0.2) ** 2 + (x[:, 1] - 0.55) ** 2) * 6)
+    y = f + noise * np.random.default_rng(seed).normal(size=len(f))
+    return spec, alpha, x, y
+
+
+@pytest.mark.parametrize("lam", [1e-6, -1.0])
+def test_tps_eval_and_refine_match_oracle(O, mc, torch, lam):
+    spec, alpha, x, y = _surface(O, 20, 0, 2e-4)
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(len(alpha), dtype=np.int32), seed=1)
+    vals = torch.tensor(y, dtype=torch.float64, device="cuda")
+    A, v, st = dsg.refine(vals, lam)
+    xs, fs, lam_o = O.refine(x, y, lam)
+    assert st[0] == 0
+    # surface parity at random points
+    fitted, w, beta = O.tps_fit(x, y, lam_o)
+    pts = np.random.default_rng(1).uniform(x.min(0), x.max(0), size=(16, 2))
+    f_gpu, g_gpu = dsg.tps_eval(0, pts)
+    for p, fg, gg in zip(pts, f_gpu, g_gpu):
+        fo, go = O.tps_eval(x, w, beta, p)
+        assert fg == pytest.approx(fo, abs=1e-9)
+        assert np.allclose(gg, go, atol=1e-7)
+    # the optimum
+    assert np.allclose(A[0, :2] / spec.alpha0, xs, atol=2e-5)
+    assert v[0] == pytest.approx(fs, abs=1e-9)
+    a3 = O.solve_alpha_n(spec.r, spec.alpha0, A[0, :2], 1e-14)
+    assert a3 == pytest.approx(A[0, 2], abs=1e-11)
+
+
+def test_refined_optimum_beats_grid_on_exact_surface(O, mc, torch):
+    """Noise-free surface of the C2 slice problem (exact P by the oracle's closed form on an m = 24 grid):
+    the continuous optimum's exact power is at least the best grid design's (within the TPS error)."""
+    spec, alpha = slice_designs(O, m=24, count=None)
+    op = oracle_problem(O, spec)
+    P = np.array([O.assurance_gaussian(op, a) for a in alpha])
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(len(alpha), dtype=np.int32), seed=1)
+    A, v, st = dsg.refine(torch.tensor(P, dtype=torch.float64, device="cuda"), 0.0)
+    assert st[0] == 0
+    assert O.fwer(spec.r, A[0]) == pytest.approx(spec.alpha0, abs=1e-11)
+    p_star = O.assurance_gaussian(op, A[0])
+    assert p_star >= P.max() - 2e-6
+    assert abs(v[0] - p_star) < 5e-5          # interpolating TPS error at the optimum
+
+
+def test_refine_passthrough_n1(O, mc, torch):
+    p = mc.problem_formula10([1.0], [0.25], 127.0)
+    dsg = mc.Design([p], [[0.025]], [0], seed=1)
+    A, v, st = dsg.refine(torch.tensor([0.68], dtype=torch.float64, device="cuda"))
+    assert st[0] == 2 and A[0, 0] == 0.025 and v[0] == 0.68
