@@ -190,6 +190,22 @@ mc_status mc_tps_eval(const mc_ctx* ctx, int32_t problem, const double* x_host, 
 mc_status mc_refine(mc_ctx* ctx, const double* values_dev, double lambda, double* alpha_out_host,
                     double* value_out_host, int32_t* status_out_host, void* cuda_stream);
 
+/* ---- NEXT f2: TPS over the r-lattice ---------------------------------------------- */
+
+typedef struct mc_surface mc_surface;
+
+/* Thin-plate spline (DESIGN.md §2.9 kernels, affine null space) through N points x_host[N*d]
+ * (1 <= d <= 3, N >= d + 2) with values y_host[N]: P:234 fits "TPS of optimal power as functions of r".
+ * lambda < 0: GCV over the §2.9 grid (influence-matrix trace); *lambda_used receives it.  Host fp64
+ * dense solve.  MC_ERR_NUMERIC if the sites are degenerate. */
+mc_status mc_surface_fit(const double* x_host, int64_t N, int32_t d, const double* y_host, double lambda,
+                         mc_surface** out, double* lambda_used);
+mc_status mc_surface_eval(const mc_surface* s, const double* x_host, int64_t q, double* f_host, double* grad_host);
+/* Maximum over the sites' bounding box by the same projected L-BFGS as mc_refine, started from the
+ * best site ("find optimal solution of r on the fitted TPS using the same procedure"). */
+mc_status mc_surface_max(const mc_surface* s, double* x_out_host, double* f_out_host);
+void mc_surface_destroy(mc_surface* s);
+
 /* ---- a10: argmax --------------------------------------------------------------- */
 
 /* Per problem: the design with the largest value (lowest index on ties; NaN never wins) ->

@@ -105,6 +105,14 @@ mc_status alpha_points_solve(const mc_problem* probs, int32_t n_probs, const int
                              double* A, uint8_t* valid);
 mc_status fwer_eval(const mc_problem* p, const double* alpha, int64_t count, double* out, int device);
 mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st);
+struct RefineOut {
+  std::vector<double> x;
+  double f = 0.0;
+  int iters = 0;
+};
+// maximise the TPS f(x) = beta0 + beta.x + sum w_i phi(|x - X_i|) over lo <= x <= hi from x0 (mc_refine.cu)
+RefineOut refine_box(const std::vector<double>& X, const std::vector<double>& w, const std::vector<double>& beta, int d,
+                     const std::vector<double>& x0, const std::vector<double>& lo, const std::vector<double>& hi);
 mc_status tps_coefficients(mc_ctx* c, const double* values, double lambda, cudaStream_t st);
 mc_status smooth_apply(mc_ctx* c, const double* values, double lambda, double* out, double* lam_used,
                        cudaStream_t st);

@@ -46,16 +46,11 @@ static double tps_value_grad(const std::vector<double>& X, const std::vector<dou
   return f;
 }
 
-struct RefineResult {
-  std::vector<double> x;
-  double f = NAN;
-  int iters = 0;
-};
 
 // maximise f over lo <= x <= hi from x0: projected L-BFGS (m = 10) with Armijo backtracking on the
 // projected path; stops on |projected gradient|_inf <= 1e-10, relative change <= 1e-15, or 500 iterations
 // (SPEC: L-BFGS-B).
-static RefineResult lbfgsb_max(const std::vector<double>& X, const std::vector<double>& w,
+RefineOut refine_box(const std::vector<double>& X, const std::vector<double>& w,
                                const std::vector<double>& beta, int d, const std::vector<double>& x0,
                                const std::vector<double>& lo, const std::vector<double>& hi) {
   const int M = 10;
@@ -136,7 +131,7 @@ static RefineResult lbfgsb_max(const std::vector<double>& X, const std::vector<d
     }
     if (change <= 1e-15 * std::max(1.0, std::fabs(gold))) { ++it; break; }
   }
-  RefineResult r;
+  RefineOut r;
   r.x = x;
   r.f = -g;
   r.iters = it;
@@ -183,7 +178,7 @@ mc_status mc_refine(mc_ctx* c, const double* values, double lambda, double* alph
   const int n = c->n, d = n - 1;
   std::vector<double> hv(c->D);
   MC_CUDA(cudaMemcpy(hv.data(), values, sizeof(double) * c->D, cudaMemcpyDeviceToHost));
-  std::vector<RefineResult> res(c->n_probs);
+  std::vector<RefineOut> res(c->n_probs);
   std::vector<int> todo;
   for (int k = 0; k < c->n_probs; ++k) {
     const int64_t b = c->prob_begin[k], e = c->prob_begin[k + 1];
@@ -214,7 +209,7 @@ mc_status mc_refine(mc_ctx* c, const double* values, double lambda, double* alph
         if (fi > bestf) { bestf = fi; for (int j = 0; j < d; ++j) x0[j] = X[i * d + j]; }
         for (int j = 0; j < d; ++j) { lo[j] = std::min(lo[j], X[i * d + j]); hi[j] = std::max(hi[j], X[i * d + j]); }
       }
-      res[k] = lbfgsb_max(X, w, beta, d, x0, lo, hi);
+      res[k] = refine_box(X, w, beta, d, x0, lo, hi);
     }
   };
   const size_t nt = std::max<size_t>(1, std::min<size_t>(todo.size(), std::thread::hardware_concurrency()));

@@ -74,6 +74,10 @@ def lib() -> ctypes.CDLL:
         L.mc_tps_fit.argtypes = [vp, vp, d, vp]; L.mc_tps_fit.restype = i32
         L.mc_tps_eval.argtypes = [vp, i32, P(d), i64, P(d), P(d)]; L.mc_tps_eval.restype = i32
         L.mc_refine.argtypes = [vp, vp, d, P(d), P(d), P(i32), vp]; L.mc_refine.restype = i32
+        L.mc_surface_fit.argtypes = [P(d), i64, i32, P(d), d, P(vp), P(d)]; L.mc_surface_fit.restype = i32
+        L.mc_surface_eval.argtypes = [vp, P(d), i64, P(d), P(d)]; L.mc_surface_eval.restype = i32
+        L.mc_surface_max.argtypes = [vp, P(d), P(d)]; L.mc_surface_max.restype = i32
+        L.mc_surface_destroy.argtypes = [vp]; L.mc_surface_destroy.restype = None
         L.mc_argmax.argtypes = [vp, vp, vp, vp, P(i64), P(d), vp]; L.mc_argmax.restype = i32
         L.mc_num_designs.argtypes = [vp]; L.mc_num_designs.restype = i64
         L.mc_num_problems.argtypes = [vp]; L.mc_num_problems.restype = i32
@@ -88,7 +92,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer", "mc_candidates",
             "mc_design_init", "mc_design_upload", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
-            "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
+            "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
 
 
@@ -345,6 +349,41 @@ class Design:
         _check(lib().mc_draw_dump(self._ctx, design.data_ptr(), sample.data_ptr(), design.numel(), out.data_ptr(),
                                   _stream(stream)))
         return out
+
+
+class Surface:
+    """NEXT f2: host TPS through arbitrary points (the optimal power over the r-lattice)."""
+
+    def __init__(self, x, y, lam: float = -1.0):
+        x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+        if x.shape[0] == 1 and np.ndim(y) and len(y) > 1:
+            x = x.T.copy()
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        self.d = x.shape[1]
+        h = ctypes.c_void_p()
+        lu = ctypes.c_double(0.0)
+        _check(lib().mc_surface_fit(_dp(x), x.shape[0], self.d, _dp(y), float(lam), ctypes.byref(h), ctypes.byref(lu)))
+        self._h, self.lam = h, lu.value
+
+    def __call__(self, x):
+        x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+        f = np.zeros(x.shape[0])
+        g = np.zeros_like(x)
+        _check(lib().mc_surface_eval(self._h, _dp(x), x.shape[0], _dp(f), _dp(g)))
+        return f, g
+
+    def maximum(self):
+        x = np.zeros(self.d)
+        f = ctypes.c_double(0.0)
+        _check(lib().mc_surface_max(self._h, _dp(x), ctypes.byref(f)))
+        return x, f.value
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().mc_surface_destroy(self._h)
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------------------------------

@@ -74,3 +74,20 @@ def test_refine_passthrough_n1(O, mc, torch):
     dsg = mc.Design([p], [[0.025]], [0], seed=1)
     A, v, st = dsg.refine(torch.tensor([0.68], dtype=torch.float64, device="cuda"))
     assert st[0] == 2 and A[0, 0] == 0.025 and v[0] == 0.68
+
+
+def test_r_sweep_surface_stage_matches_oracle(O, mc, torch):
+    """NEXT f2 on a reduced lattice (scenario (c), step 0.1 -> 36 r-pairs, m = 12 grid, 2e4 draws): the
+    per-problem optima come from the library; the TPS over r and its maximum must equal the oracle's
+    (scipy L-BFGS-B on the oracle TPS) on the same points; the optimal powers lie in [0, 1]."""
+    from paper_2005_10494_b200 import sweep
+    specs = [W.ProblemSpec(r=(1.0, a, b), scenario="c", i3=211.0) for a, b in W.r_lattice(0.1)]
+    assert len(specs) == 36
+    probs = [lib_problem(mc, s) for s in specs]
+    res = sweep.sweep(probs, m=12, n3=0, seed=W.SEED, total_samples=20_000, lam_r=-1.0)
+    assert np.all(res.status != 1)
+    assert np.all((res.power_opt > 0.5) & (res.power_opt < 1.0))
+    xs, fs, lam = O.refine(res.r, res.power_opt, -1.0)
+    assert res.lambda_r == pytest.approx(lam, rel=1e-9)
+    assert np.allclose(res.r_star, xs, atol=1e-5)
+    assert res.power_r_star == pytest.approx(fs, abs=1e-9)

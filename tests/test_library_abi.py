@@ -119,3 +119,24 @@ def test_shard_range_partitions(mc):
             for (b0, c0), (b1, _) in zip(rs, rs[1:]):
                 assert b0 + c0 == b1 and b1 % 64 == 0
             assert rs[-1][0] + rs[-1][1] == total
+
+
+def test_host_surface_matches_oracle_tps(mc, O):
+    """The host TPS over arbitrary points (NEXT f2) against the oracle: values, GCV lambda, maximum."""
+    rng = np.random.default_rng(0)
+    x = rng.uniform(0, 1, (40, 2))
+    y = np.exp(-((x - 0.4) ** 2).sum(1) * 3) + 0.01 * rng.normal(size=40)
+    for lam in (0.0, 1e-4, -1.0):
+        s = mc.Surface(x, y, lam)
+        ref, lr = O.tps_smooth(x, y, lam)
+        assert s.lam == pytest.approx(lr, rel=1e-12)
+        f, _ = s(x)
+        assert np.allclose(f, ref, atol=1e-9)
+        xs, fs = s.maximum()
+        xo, fo, _ = O.refine(x, y, lr)
+        assert np.allclose(xs, xo, atol=1e-6) and fs == pytest.approx(fo, abs=1e-9)
+    # d = 1 (cubic) as well
+    x1 = np.linspace(0, 1, 12)[:, None]
+    y1 = np.sin(3 * x1[:, 0])
+    s1 = mc.Surface(x1, y1, 0.0)
+    assert np.allclose(s1(x1)[0], y1, atol=1e-10)
