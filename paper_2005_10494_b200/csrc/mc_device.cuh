@@ -105,6 +105,22 @@ __device__ __forceinline__ void philox_block_rk(uint64_t q, uint32_t lo1d, uint3
   out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
+// Block for counter (q_lo, q_hi, design, 0) when the caller holds the round-1 word
+// c0 = hi(M1 * design) ^ q_hi ^ k0 fixed (q_hi constant over a thread's run): one IMAD.WIDE and one
+// LOP3 in round 1 instead of two each.
+__device__ __forceinline__ void philox_block_lo(uint32_t q0, uint32_t c0r1, uint32_t lo1d, const RoundKeys& rk,
+                                                uint32_t out[4]) {
+  uint32_t hq, lq;
+  mulhilo(q0, 0xD2511F53u, hq, lq);
+  uint32_t c0 = c0r1;
+  uint32_t c1 = lo1d;
+  uint32_t c2 = hq ^ rk.k1[0];
+  uint32_t c3 = lq;
+#pragma unroll
+  for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
 __device__ __forceinline__ uint32_t philox_word(uint64_t seed, uint32_t design, uint64_t w) {
   Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
   uint32_t o[4];
@@ -240,33 +256,36 @@ __device__ __forceinline__ float normal_quantile(float p, float pc) {
 #endif
 __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
   constexpr double S2 = 1.4142135623730950488;
-  const float w = -0.69314718056f * (lg2_approx(fmaxf(p * pc, 1.0e-38f)) + 2.0f);
+  // p pc may flush to 0 (e ~ 0): lg2 -> -inf, w -> +inf, handled by the deep-tail clamp
+  const float w = -0.69314718056f * (lg2_approx(p * pc) + 2.0f);
 #if MC_QUANTILE_BRANCHFREE
-  // all three polynomials with selects: one basic block (the scheduler can interleave across draws)
-  const float ww = w - 2.5f;
-  float g = (float)(2.81022636e-08 * S2);
-  g = fmaf(g, ww, (float)(3.43273939e-07 * S2));
-  g = fmaf(g, ww, (float)(-3.5233877e-06 * S2));
-  g = fmaf(g, ww, (float)(-4.39150654e-06 * S2));
-  g = fmaf(g, ww, (float)(0.00021858087 * S2));
-  g = fmaf(g, ww, (float)(-0.00125372503 * S2));
-  g = fmaf(g, ww, (float)(-0.00417768164 * S2));
-  g = fmaf(g, ww, (float)(0.246640727 * S2));
-  g = fmaf(g, ww, (float)(1.50140941 * S2));
-  const float sw = sqrt_approx(fminf(w, 88.0f));
-  const bool deep = w >= 16.0f;
-  // tail and deep tail share one Horner chain with selected coefficients
-  const float wt = deep ? sw - 6.0f : sw - 3.0f;
-  float gt = deep ? 0.0f : (float)(-0.000200214257 * S2);
-  gt = fmaf(gt, wt, deep ? 0.0f : (float)(0.000100950558 * S2));
-  gt = fmaf(gt, wt, deep ? (float)(7.926354328446905e-07 * S2) : (float)(0.00134934322 * S2));
-  gt = fmaf(gt, wt, deep ? (float)(-6.932396900083404e-06 * S2) : (float)(-0.00367342844 * S2));
-  gt = fmaf(gt, wt, deep ? (float)(2.5214179913746193e-05 * S2) : (float)(0.00573950773 * S2));
-  gt = fmaf(gt, wt, deep ? (float)(-3.964155257563107e-05 * S2) : (float)(-0.0076224613 * S2));
-  gt = fmaf(gt, wt, deep ? (float)(-0.0004801170143764466 * S2) : (float)(0.00943887047 * S2));
-  gt = fmaf(gt, wt, deep ? (float)(1.0096029043197632 * S2) : (float)(1.00167406 * S2));
-  gt = fmaf(gt, wt, deep ? (float)(5.859915256500244 * S2) : (float)(2.83297682 * S2));
-  g = w < 5.0f ? g : gt;
+  // w in [0, 16) (p in [1.1e-7, 1 - 1.1e-7]): ONE degree-12 polynomial in sqrt(w + 2)
+  // (tools/fit_erfinv_single.py, relative error 5.3e-7 in fp32) -- no per-coefficient selects on the
+  // ALU pipe; the deep tail w >= 16 (e_i < ~1e-7) takes a rare divergent branch.
+  const float x = sqrt_approx(w + 2.0f) - 2.82842712474619f;
+  float g = -0.0001458914359425521f;
+  g = fmaf(g, x, 0.00014054195626482066f);
+  g = fmaf(g, x, 0.0012376677239334937f);
+  g = fmaf(g, x, -0.0017637622021570974f);
+  g = fmaf(g, x, -0.0036462519812319317f);
+  g = fmaf(g, x, 0.009457966527136036f);
+  g = fmaf(g, x, -0.0013609513949184736f);
+  g = fmaf(g, x, -0.022852510105916587f);
+  g = fmaf(g, x, 0.04599717902636056f);
+  g = fmaf(g, x, -0.040789581299890895f);
+  g = fmaf(g, x, -0.018363709814932894f);
+  g = fmaf(g, x, 1.59782737417905f);
+  g = fmaf(g, x, 3.2334928032079135f);
+  if (w >= 16.0f) {
+    const float ww = sqrt_approx(fminf(w, 88.0f)) - 6.0f;
+    g = (float)(7.926354328446905e-07 * S2);
+    g = fmaf(g, ww, (float)(-6.932396900083404e-06 * S2));
+    g = fmaf(g, ww, (float)(2.5214179913746193e-05 * S2));
+    g = fmaf(g, ww, (float)(-3.964155257563107e-05 * S2));
+    g = fmaf(g, ww, (float)(-0.0004801170143764466 * S2));
+    g = fmaf(g, ww, (float)(1.0096029043197632 * S2));
+    g = fmaf(g, ww, (float)(5.859915256500244 * S2));
+  }
   return g * (p - pc);
 #else
   float g;

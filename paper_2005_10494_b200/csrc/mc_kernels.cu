@@ -68,6 +68,27 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
   static_assert(SAMPLES_PER_THREAD % G::L == 0, "L must divide the per-thread run");
   uint64_t q = s_begin * (uint64_t)G::U / 4;   // first Philox block of this thread's run
   const uint32_t one = one_bits_reg();
+  if constexpr (!MASKED) {
+    // steady state: the run's Philox counters q .. q + STEPS*BLOCKS share q_hi unless the low word wraps
+    constexpr uint32_t NBLK = (uint32_t)(STEPS * G::BLOCKS);
+    const uint32_t q0 = (uint32_t)q;
+    if (q0 <= 0xFFFFFFFFu - NBLK) {
+      const uint32_t c0r1 = hi1d ^ (uint32_t)(q >> 32) ^ rk.k0[0];
+      uint32_t ql = q0;
+#pragma unroll 1
+      for (int st = 0; st < STEPS; ++st) {
+        uint32_t w[G::BLOCKS * 4];
+#pragma unroll
+        for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk, &w[4 * b]);
+        ql += G::BLOCKS;
+#pragma unroll
+        for (int l = 0; l < G::L; ++l)
+          accumulate<EST>(draw_utility<N, EST, false, MODEL>(&w[l * G::U], one, zc, pr, nullptr, nullptr, &sr), a1, a2);
+      }
+      if constexpr (EST == 1) a2 = a1;
+      return;
+    }
+  }
 #pragma unroll 1
   for (int st = 0; st < STEPS; ++st) {
     const uint64_t s0 = s_begin + (uint64_t)st * G::L;
@@ -93,7 +114,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
 // independent (no block barrier): each reduces its tile with 64-bit shuffles and lane 0 issues one
 // 64-bit atomicAdd pair.  Warp tiles are strided over the persistent grid's warps.
 constexpr int min_blocks(int n, int est, int model) {
-  return model == 1 ? 3 : (n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1));
+  return model == 1 ? 2 : (n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1));
 }
 
 template <int N, int EST, int MODEL>
