@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--est", choices=["cond", "ind"], default="cond")
+    ap.add_argument("--crn", action="store_true", help="NEXT f3: common random numbers per problem (not the headline)")
     ap.add_argument("--draws", type=int, default=W.DRAWS["C2"], help="draws per design per step (all ranks)")
     ap.add_argument("--problems", type=int, default=0, help="limit the C2 problem list (0 = all 513)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -147,6 +148,8 @@ def run_ours(args):
     alpha, pod = mc.candidates(problems, m=W.GRID_M, n3=W.N3, seed=W.SEED, device=local)
     t_cand = time.perf_counter() - t_prep0
     design = mc.Design(problems, alpha, pod, seed=W.SEED, estimator=est, device=local)
+    if args.crn:
+        design.set_sampling(True)
     t1 = time.perf_counter()
     design.smooth_plan()
     torch.cuda.synchronize()
@@ -238,11 +241,12 @@ def run_ours(args):
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     mhz = clk.get("sm_mhz") or 1965.0
     peak = ISSUE_LANES_PER_CLK_PER_SM * sm_count * (clk.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12   # T lane-instr/s
-    ipd = issue_per_draw(args.est)
+    ipd = issue_per_draw(args.est) if not args.crn else float("nan")
     achieved = ipd * draws_launch / (kms * 1e-3) / 1e12
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "Tinst/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": f"mc_fused_kernel<3,{0 if est == 0 else 1}>", "kernel_ms": round(kms, 3),
+            "kernel": ("mc_crn_kernel" if args.crn else "mc_fused_kernel") + f"<3,{0 if est == 0 else 1},0>",
+            "kernel_ms": round(kms, 3),
             "kernel_share_of_step": round(kms / (ms / args.steps), 4),
             "issue_per_draw": ipd,
             "peak_basis": "128 lane-instr/clk/SM x SMs x sm_max_mhz (DESIGN.md §4)",
@@ -263,6 +267,7 @@ def run_ours(args):
                 "dtype": "f32 per-draw / int64 sums / f64 finalize+TPS", "data": "synthetic",
                 "config": {"workload": "C2: paper 3-D problem (513 r-problems x 2000 alpha designs), 1e6 draws/design",
                            "problems": len(specs), "designs": D, "draws_per_design": N, "estimator": args.est,
+                           "sampling": "common random numbers per problem" if args.crn else "independent per design",
                            "seed": W.SEED, "parallelism": f"sample-shard x{world} + int64 all_reduce",
                            "l2": "no flush: the per-step TPS plan read (~%.1f GB) exceeds L2" % (
                                8.0 * sum((pod == k).sum() ** 2 for k in range(len(specs))) / 1e9)},

@@ -129,6 +129,12 @@ mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs,
  * the new alpha equals the previous table (the TPS sites are unchanged), else it is invalidated. */
 mc_status mc_design_upload(mc_ctx* ctx, const double* alpha_host, void* cuda_stream);
 
+/* Sampling mode (NEXT f3): 0 = independent draws per design (stream keyed (design, sample), tag 0;
+ * the default, reading R2); 1 = common random numbers per problem (stream keyed (problem, sample),
+ * counter word 3 = 1): every design of a problem sees the same draws, so design differences have far
+ * less noise and the draw's design-independent work is shared by blocks of 8 designs.  n <= 3. */
+mc_status mc_set_sampling(mc_ctx* ctx, int32_t mode);
+
 /* Launch shape of the fused kernel (results do not depend on it): threads per block (multiple of
  * 32 in [32, 256]; 0 = default 256) and grid blocks (>= 0; 0 = #SMs x max resident blocks). */
 mc_status mc_set_launch(mc_ctx* ctx, int32_t block_threads, int32_t grid_blocks);

@@ -55,6 +55,18 @@ void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32
 
 /* Word w of design d's stream: block q = w/4 with counter
  * (q_lo, q_hi, d, 0) and key (seed_lo, seed_hi); the word is lane w mod 4.   */
+uint32_t or_word_tagged(uint64_t seed, uint32_t id, uint32_t tag, uint64_t w)
+{
+    uint64_t q = w / 4;
+    uint32_t ctr[4] = { (uint32_t)q, (uint32_t)(q >> 32), id, tag };
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint32_t out[4];
+    or_philox4x32_10(ctr, key, out);
+    return out[w % 4];
+}
+
+/* Stream tags: tag 0 = independent draws per design (id = design index), tag 1 = common
+ * random numbers per problem (id = problem index; NEXT f3).  The draw functions below take (id, tag). */
 uint32_t or_word(uint64_t seed, uint32_t design, uint64_t w)
 {
     uint64_t q = w / 4;
@@ -174,11 +186,11 @@ int or_words_per_draw(int n, int p, int est)
 }
 
 /* Box-Muller: pair j uses words 2j (radius) and 2j+1 (angle) of the draw. */
-static void bm_normals(uint64_t seed, uint32_t design, uint64_t w0, int nnorm, double *normals)
+static void bm_normals(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0, int nnorm, double *normals)
 {
     for (int j = 0; 2 * j < nnorm; ++j) {
-        double R = sqrt(-2.0 * log(u_radius(or_word(seed, design, w0 + 2 * j))));
-        double a = 2.0 * M_PI * u_angle(or_word(seed, design, w0 + 2 * j + 1));
+        double R = sqrt(-2.0 * log(u_radius(or_word_tagged(seed, design, tag, w0 + 2 * j))));
+        double a = 2.0 * M_PI * u_angle(or_word_tagged(seed, design, tag, w0 + 2 * j + 1));
         normals[2 * j] = R * cos(a);
         normals[2 * j + 1] = R * sin(a);
     }
@@ -187,7 +199,7 @@ static void bm_normals(uint64_t seed, uint32_t design, uint64_t w0, int nnorm, d
 /* Utility of one draw given the thresholds b of Phi_Sigma0 (Formulas 4-7):
  * IND uses the null normals w[0..n); COND reads its uniforms at word vw0 + a. */
 static double utility_from_b(int n, const double *r, const double *b, const double *w, int est,
-                             uint64_t seed, uint32_t design, uint64_t vw0, double *wnull_out)
+                             uint64_t seed, uint32_t design, uint32_t tag, uint64_t vw0, double *wnull_out)
 {
     double S0[OR_MAXN * OR_MAXN], L0[OR_MAXN * OR_MAXN];
     or_null_corr(n, r, S0);
@@ -235,7 +247,7 @@ static double utility_from_b(int n, const double *r, const double *b, const doub
         prod *= e;
         if (prod == 0.0) break;                        /* u = 1 exactly; later stages are irrelevant */
         if (a < neven) {
-            double v = u_open(or_word(seed, design, vw0 + a));
+            double v = u_open(or_word_tagged(seed, design, tag, vw0 + a));
             y[a] = or_Phi_inv(v * e);
         }
     }
@@ -244,14 +256,14 @@ static double utility_from_b(int n, const double *r, const double *b, const doub
 
 
 double or_draw(int n, int p, const double *r, double i3, const double *theta, const double *Lp,
-               const double *z, int est, uint64_t seed, uint32_t design, uint64_t s,
+               const double *z, int est, uint64_t seed, uint32_t design, uint32_t tag, uint64_t s,
                double *eps_out, double *delta_out, double *b_out, double *wnull_out)
 {
     const int U = or_words_per_draw(n, p, est);
     const uint64_t w0 = s * (uint64_t)U;
     const int nnorm = (est == 0) ? p : p + n;
     double normals[2 * OR_MAXN + 2];
-    bm_normals(seed, design, w0, nnorm, normals);
+    bm_normals(seed, design, tag, w0, nnorm, normals);
     /* Formula 10: Delta = theta + Lp * eps. */
     double delta[OR_MAXN], b[OR_MAXN];
     for (int i = 0; i < n; ++i) {
@@ -264,7 +276,7 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
     if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
     if (delta_out) for (int i = 0; i < n; ++i) delta_out[i] = delta[i];
     if (b_out) for (int i = 0; i < n; ++i) b_out[i] = b[i];
-    return utility_from_b(n, r, b, normals + p, est, seed, design, w0 + 2 * ((p + 1) / 2), wnull_out);
+    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, w0 + 2 * ((p + 1) / 2), wnull_out);
 }
 
 /* C4 strata prior (a synthetic extension inside the Formula-3 model, not in the paper).
@@ -276,7 +288,7 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
  *   Delta_2 = q+ delta+ + (1 - q+) delta-,  Delta_neg = q- delta+ + (1 - q-) delta-,
  *   Delta_1 = r2 Delta_2 + (1 - r2) Delta_neg;  mu_i = sqrt(r_i I_eff) Delta_i;  b = z - mu.      */
 double or_draw_strata(double r2, double i3, const double *sp, const double *z, int est, uint64_t seed,
-                      uint32_t design, uint64_t s, double *eps_out, double *delta_out, double *b_out,
+                      uint32_t design, uint32_t tag, uint64_t s, double *eps_out, double *delta_out, double *b_out,
                       double *wnull_out)
 {
     const int n = 2, p = 5;
@@ -284,7 +296,7 @@ double or_draw_strata(double r2, double i3, const double *sp, const double *z, i
     const int U = or_words_per_draw(n, p, est);
     const uint64_t w0 = s * (uint64_t)U;
     double normals[2 * OR_MAXN + 2];
-    bm_normals(seed, design, w0, est == 0 ? p : p + n, normals);
+    bm_normals(seed, design, tag, w0, est == 0 ? p : p + n, normals);
     const double pi = 1.0 / (1.0 + exp(-(sp[0] + sp[1] * normals[0])));
     const double dp = sp[2] + sp[3] * normals[1];
     const double dm = sp[4] + sp[5] * normals[2];
@@ -302,15 +314,15 @@ double or_draw_strata(double r2, double i3, const double *sp, const double *z, i
     if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
     if (delta_out) { delta_out[0] = d1; delta_out[1] = d2; }
     if (b_out) { b_out[0] = b[0]; b_out[1] = b[1]; }
-    return utility_from_b(n, r, b, normals + p, est, seed, design, w0 + 2 * ((p + 1) / 2), wnull_out);
+    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, w0 + 2 * ((p + 1) / 2), wnull_out);
 }
 
 void or_design_sums_strata(double r2, double i3, const double *sp, const double *z, int est, uint64_t seed,
-                           uint32_t design, uint64_t s0, uint64_t count, int64_t *sums)
+                           uint32_t design, uint32_t tag, uint64_t s0, uint64_t count, int64_t *sums)
 {
     int64_t a1 = 0, a2 = 0;
     for (uint64_t s = s0; s < s0 + count; ++s) {
-        double u = or_draw_strata(r2, i3, sp, z, est, seed, design, s, NULL, NULL, NULL, NULL);
+        double u = or_draw_strata(r2, i3, sp, z, est, seed, design, tag, s, NULL, NULL, NULL, NULL);
         a1 += (int64_t)nearbyint(ldexp(u, 23));
         a2 += (int64_t)nearbyint(ldexp(u * u, 23));
     }
@@ -321,12 +333,12 @@ void or_design_sums_strata(double r2, double i3, const double *sp, const double 
 /* Per-design sums over samples [s0, s0+count): each draw's u
  * and u^2 are rounded (half-to-even) to the 2^-23 grid and added as integers.  */
 void or_design_sums(int n, int p, const double *r, double i3, const double *theta, const double *Lp,
-                    const double *z, int est, uint64_t seed, uint32_t design,
+                    const double *z, int est, uint64_t seed, uint32_t design, uint32_t tag,
                     uint64_t s0, uint64_t count, int64_t *sums)
 {
     int64_t a1 = 0, a2 = 0;
     for (uint64_t s = s0; s < s0 + count; ++s) {
-        double u = or_draw(n, p, r, i3, theta, Lp, z, est, seed, design, s, NULL, NULL, NULL, NULL);
+        double u = or_draw(n, p, r, i3, theta, Lp, z, est, seed, design, tag, s, NULL, NULL, NULL, NULL);
         a1 += (int64_t)nearbyint(ldexp(u, 23));
         a2 += (int64_t)nearbyint(ldexp(u * u, 23));
     }

@@ -53,19 +53,21 @@ def lib():
         L.or_cholesky.argtypes = [i32, P(d), P(d)]; L.or_cholesky.restype = i32
         L.or_null_corr.argtypes = [i32, P(d), P(d)]
         L.or_words_per_draw.argtypes = [i32, i32, i32]; L.or_words_per_draw.restype = i32
-        L.or_draw.argtypes = [i32, i32, P(d), d, P(d), P(d), P(d), i32, u64, u32, u64,
+        L.or_word_tagged.argtypes = [u64, u32, u32, u64]
+        L.or_word_tagged.restype = u32
+        L.or_draw.argtypes = [i32, i32, P(d), d, P(d), P(d), P(d), i32, u64, u32, u32, u64,
                               P(d), P(d), P(d), P(d)]
         L.or_draw.restype = d
-        L.or_design_sums.argtypes = [i32, i32, P(d), d, P(d), P(d), P(d), i32, u64, u32, u64, u64, P(i64)]
+        L.or_design_sums.argtypes = [i32, i32, P(d), d, P(d), P(d), P(d), i32, u64, u32, u32, u64, u64, P(i64)]
         L.or_mvn_orthant.argtypes = [i32, P(d), P(d)]; L.or_mvn_orthant.restype = d
         L.or_fwer.argtypes = [i32, P(d), P(d)]; L.or_fwer.restype = d
         L.or_solve_alpha_n.argtypes = [i32, P(d), d, P(d), d, P(d)]; L.or_solve_alpha_n.restype = i32
         L.or_alpha_grid.argtypes = [i32, P(d), d, i32, d, P(d), P(ctypes.c_uint8)]
         L.or_alpha_grid.restype = i64
         L.or_subset.argtypes = [i64, i64, u64, P(i64)]
-        L.or_draw_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u64, P(d), P(d), P(d), P(d)]
+        L.or_draw_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u32, u64, P(d), P(d), P(d), P(d)]
         L.or_draw_strata.restype = d
-        L.or_design_sums_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u64, u64, P(i64)]
+        L.or_design_sums_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u32, u64, u64, P(i64)]
         _lib = L
     return _lib
 
@@ -194,26 +196,29 @@ def thresholds(alpha) -> np.ndarray:
     return np.array([threshold(a) for a in np.asarray(alpha, dtype=np.float64)])
 
 
-def draw(prob: Problem, alpha, est: int, seed: int, design: int, s: int) -> dict:
-    """One draw: returns the prior normals, Delta, b and u (for per-draw parity)."""
+def draw(prob: Problem, alpha, est: int, seed: int, design: int, s: int, tag: int = 0) -> dict:
+    """One draw: returns the prior normals, Delta, b and u (for per-draw parity).  tag 0: the stream of
+    `design`; tag 1: the common-random-number stream of problem `design` (NEXT f3)."""
     n = prob.n
     p = n
     z = thresholds(alpha)
     eps, delta, b, wn = np.zeros(p), np.zeros(n), np.zeros(n), np.zeros(n)
     P = ctypes.POINTER(ctypes.c_double)
     u = lib().or_draw(n, p, _dp(prob.r), prob.i3, _dp(prob.theta), _dp(prob.Lp), _dp(z), est,
-                      seed, design, s, eps.ctypes.data_as(P), delta.ctypes.data_as(P),
+                      seed, design, tag, s, eps.ctypes.data_as(P), delta.ctypes.data_as(P),
                       b.ctypes.data_as(P), wn.ctypes.data_as(P))
     return {"u": float(u), "eps": eps, "delta": delta, "b": b, "xnull": wn}
 
 
-def design_sums(prob: Problem, alpha, est: int, seed: int, design: int, s0: int, count: int) -> np.ndarray:
-    """Integer sums (sum q(u), sum q(u^2)) over samples [s0, s0+count), q = round(2^23 x)."""
+def design_sums(prob: Problem, alpha, est: int, seed: int, design: int, s0: int, count: int,
+                tag: int = 0) -> np.ndarray:
+    """Integer sums (sum q(u), sum q(u^2)) over samples [s0, s0+count), q = round(2^23 x).  With tag 1
+    `design` is the problem index of the common-random-number stream (NEXT f3)."""
     n = prob.n
     z = thresholds(alpha)
     sums = np.zeros(2, dtype=np.int64)
     lib().or_design_sums(n, n, _dp(prob.r), prob.i3, _dp(prob.theta), _dp(prob.Lp), _dp(z), est, seed,
-                         design, s0, count, sums.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+                         design, tag, s0, count, sums.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
     return sums
 
 
@@ -401,22 +406,22 @@ def argmax(values) -> int:
 # --------------------------------------------------------------------------------------
 # C4: 5-D strata prior (synthetic extension of Formula 3, see oracle.c)
 
-def draw_strata(r2: float, i3: float, sp, alpha, est: int, seed: int, design: int, s: int) -> dict:
+def draw_strata(r2: float, i3: float, sp, alpha, est: int, seed: int, design: int, s: int, tag: int = 0) -> dict:
     z = thresholds(alpha)
     eps, delta, b, wn = np.zeros(5), np.zeros(2), np.zeros(2), np.zeros(2)
     P = ctypes.POINTER(ctypes.c_double)
     u = lib().or_draw_strata(float(r2), float(i3), _dp(np.asarray(sp, dtype=np.float64)), _dp(z), est, seed, design,
-                             s, eps.ctypes.data_as(P), delta.ctypes.data_as(P), b.ctypes.data_as(P),
+                             tag, s, eps.ctypes.data_as(P), delta.ctypes.data_as(P), b.ctypes.data_as(P),
                              wn.ctypes.data_as(P))
     return {"u": float(u), "eps": eps, "delta": delta, "b": b, "xnull": wn}
 
 
 def design_sums_strata(r2: float, i3: float, sp, alpha, est: int, seed: int, design: int, s0: int,
-                       count: int) -> np.ndarray:
+                       count: int, tag: int = 0) -> np.ndarray:
     z = thresholds(alpha)
     sums = np.zeros(2, dtype=np.int64)
     lib().or_design_sums_strata(float(r2), float(i3), _dp(np.asarray(sp, dtype=np.float64)), _dp(z), est, seed,
-                                design, s0, count, sums.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+                                design, tag, s0, count, sums.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
     return sums
 
 

@@ -407,6 +407,13 @@ mc_status mc_design_upload(mc_ctx* c, const double* alpha, void* stream) {
   return launch_zc(c, (cudaStream_t)stream);
 }
 
+mc_status mc_set_sampling(mc_ctx* c, int32_t mode) {
+  if (!c || (mode != 0 && mode != 1)) { set_error("mc_set_sampling: mode must be 0 (independent) or 1 (CRN)"); return MC_ERR_INVALID; }
+  if (mode == 1 && c->n > 3) { set_error("mc_set_sampling: common random numbers are built for n <= 3"); return MC_ERR_INVALID; }
+  c->sampling = mode;
+  return MC_OK;
+}
+
 mc_status mc_set_launch(mc_ctx* c, int32_t threads, int32_t grid) {
   if (!c) { set_error("mc_set_launch: null ctx"); return MC_ERR_INVALID; }
   if (threads == 0) threads = 256;
@@ -428,6 +435,7 @@ void mc_destroy(mc_ctx* c) {
     cudaFree(pl.d_lam);
   }
   cudaFree(c->d_tps_scratch);
+  cudaFree(c->d_crn);
   cudaFree(c->d_prob);
   cudaFree(c->d_zc);
   cudaFree(c->d_alpha);

@@ -108,13 +108,14 @@ __device__ __forceinline__ void philox_block_rk(uint64_t q, uint32_t lo1d, uint3
 // Block for counter (q_lo, q_hi, design, 0) when the caller holds the round-1 word
 // c0 = hi(M1 * design) ^ q_hi ^ k0 fixed (q_hi constant over a thread's run): one IMAD.WIDE and one
 // LOP3 in round 1 instead of two each.
-__device__ __forceinline__ void philox_block_lo(uint32_t q0, uint32_t c0r1, uint32_t lo1d, const RoundKeys& rk,
-                                                uint32_t out[4]) {
+// k1r1 = k1 ^ c3 of round 1 (c3 = the stream tag: 0 independent, 1 common random numbers).
+__device__ __forceinline__ void philox_block_lo(uint32_t q0, uint32_t c0r1, uint32_t lo1d, uint32_t k1r1,
+                                                const RoundKeys& rk, uint32_t out[4]) {
   uint32_t hq, lq;
   mulhilo(q0, 0xD2511F53u, hq, lq);
   uint32_t c0 = c0r1;
   uint32_t c1 = lo1d;
-  uint32_t c2 = hq ^ rk.k1[0];
+  uint32_t c2 = hq ^ k1r1;
   uint32_t c3 = lq;
 #pragma unroll
   for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
@@ -125,6 +126,19 @@ __device__ __forceinline__ uint32_t philox_word(uint64_t seed, uint32_t design, 
   Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
   uint32_t o[4];
   philox_block(w >> 2, 0xCD9E8D57u * design, __umulhi(0xCD9E8D57u, design), key, o);
+  return o[w & 3];
+}
+
+// Word w of the stream (id, tag): counter (q_lo, q_hi, id, tag) — plain 10-round form (test hooks).
+__device__ __forceinline__ uint32_t philox_word_tagged(uint64_t seed, uint32_t id, uint32_t tag, uint64_t w) {
+  uint32_t c0 = (uint32_t)(w >> 2), c1 = (uint32_t)(w >> 34), c2 = id, c3 = tag;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    philox_round(c0, c1, c2, c3, k0, k1);
+  }
+  const uint32_t o[4] = {c0, c1, c2, c3};
   return o[w & 3];
 }
 
@@ -377,42 +391,71 @@ __device__ __forceinline__ void strata_b(const float* nrm, const float* zc, cons
   b[1] = fmaf(-si * s.sqrt_r2 * s.rs1, d2, zc[1]);
 }
 
-template <int N, int EST, bool DBG, int MODEL = 0>
-__device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, const float* zc, const ProbRegs<N>& pr,
-                                              float* dbg = nullptr, const float* bsc = nullptr,
-                                              const StrataRegs* sr = nullptr) {
+// The design-independent part of one draw (shared by every design under common random numbers,
+// NEXT f3): the prior term v with b = zc - v, the IND null vector X, and the SOV uniforms.
+template <int N, int EST, int MODEL = 0>
+struct Shared {
+  float v[N];
+  float x[EST == 1 ? N : 1];                                   // IND: X = L0 W (scaled)
+  float vu[Geo<N, EST, MODEL>::NE > 0 ? Geo<N, EST, MODEL>::NE : 1];   // COND: SOV uniforms v_k
+};
+
+template <int N, int EST, int MODEL>
+__device__ __forceinline__ void draw_shared(const uint32_t* w, uint32_t one, const ProbRegs<N>& pr,
+                                            const StrataRegs* sr, Shared<N, EST, MODEL>& sh, float* nrm_out = nullptr) {
   using G = Geo<N, EST, MODEL>;
   float nrm[2 * G::NPAIR];
 #pragma unroll
   for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(w[2 * j], w[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
-  float b[N];
+  if (nrm_out)
+#pragma unroll
+    for (int k = 0; k < G::NNORM; ++k) nrm_out[k] = nrm[k];
   if constexpr (MODEL == 1) {
     static_assert(N == 2, "the C4 strata model has n = 2");
-    strata_b(nrm, zc, *sr, b);
+    const float zero[2] = {0.0f, 0.0f};
+    float bb[2];
+    strata_b(nrm, zero, *sr, bb);
+    sh.v[0] = -bb[0];
+    sh.v[1] = -bb[1];
   } else {
-    // b_i = z_i - c_i Delta_i = (z_i - c_i theta_i) - sum_{j<=i} (c_i L_p,ij) eps_j   (Formulas 3-5, 10)
+    // c_i Delta_i - c_i theta_i = sum_{j<=i} (c_i L_p,ij) eps_j   (Formulas 3-5, 10)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      float acc = zc[i];
+      float acc = 0.0f;
 #pragma unroll
-      for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
-      b[i] = acc;
+      for (int j = 0; j <= i; ++j) acc = fmaf(pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
+      sh.v[i] = acc;
     }
   }
-  float u = 0.0f;
   if constexpr (EST == 1) {
-    // Formula 6/7: one null draw X = L0 W (Markov recursion), success iff some X_i > b_i.
+    // Formula 6/7: the null draw X = L0 W by the Markov recursion
     float x = nrm[G::P];
-    bool rej = x > b[0];
+    sh.x[0] = x;
 #pragma unroll
     for (int i = 1; i < N; ++i) {
       x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * nrm[G::P + i]);
-      rej = rej || (x > b[i]);
+      sh.x[i] = x;
     }
+  } else {
+    constexpr int VB = 2 * ((G::P + 1) / 2);
+#pragma unroll
+    for (int k = 0; k < G::NE; ++k) sh.vu[k] = word_to_f12(w[VB + k], one) - 0.99999994039535522f;  // (k+1/2) 2^-23
+  }
+}
+
+// The design-dependent part: the utility u in [0, 1] from the thresholds b (= zc - v).
+template <int N, int EST, int MODEL>
+__device__ __forceinline__ float utility_of_b(const float* b, const Shared<N, EST, MODEL>& sh, const ProbRegs<N>& pr) {
+  using G = Geo<N, EST, MODEL>;
+  float u = 0.0f;
+  if constexpr (EST == 1) {
+    // success iff some X_i > b_i
+    bool rej = sh.x[0] > b[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) rej = rej || (sh.x[i] > b[i]);
     u = rej ? 1.0f : 0.0f;
   } else {
     // COND: u = 1 - prod e accumulated as u <- u + (1 - u) q (q = 1 - e: no cancellation).
-    constexpr int VB = 2 * ((G::P + 1) / 2);
     float x[G::NE > 0 ? G::NE : 1];
     float q, e;
 #pragma unroll
@@ -420,7 +463,7 @@ __device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, c
       const float a = k == 0 ? b[1] : fmaf(-pr.er[k], x[k - 1], b[2 * k + 1]);
       normal_tail(a, q, e);
       u = k == 0 ? q : fmaf(1.0f - u, q, u);
-      const float v = word_to_f12(w[VB + k], one) - 0.99999994039535522f;   // (k + 1/2) 2^-23
+      const float v = sh.vu[k];
       const float vc = 1.0f - v;                                            // exact
       const float y = normal_quantile_fast(v * e, fmaf(v, q, vc));
       x[k] = k == 0 ? y : fmaf(pr.esd[k], y, pr.emu[k] * x[k - 1]);
@@ -434,6 +477,47 @@ __device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, c
       u = (G::NE == 0 && j == 0) ? q : fmaf(1.0f - u, q, u);
     }
   }
+  return u;
+}
+
+// Independent draws: b is formed directly from zc (FFMA chains seeded with zc, no separate v).
+template <int N, int EST, bool DBG, int MODEL = 0>
+__device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, const float* zc, const ProbRegs<N>& pr,
+                                              float* dbg = nullptr, const float* bsc = nullptr,
+                                              const StrataRegs* sr = nullptr) {
+  using G = Geo<N, EST, MODEL>;
+  Shared<N, EST, MODEL> sh;
+  float nrm[2 * G::NPAIR];
+  float b[N];
+  if constexpr (MODEL == 1) {
+    draw_shared<N, EST, MODEL>(w, one, pr, sr, sh, nrm);
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = zc[i] - sh.v[i];
+  } else {
+#pragma unroll
+    for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(w[2 * j], w[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      float acc = zc[i];
+#pragma unroll
+      for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
+      b[i] = acc;
+    }
+    if constexpr (EST == 1) {
+      float x = nrm[G::P];
+      sh.x[0] = x;
+#pragma unroll
+      for (int i = 1; i < N; ++i) {
+        x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * nrm[G::P + i]);
+        sh.x[i] = x;
+      }
+    } else {
+      constexpr int VB = 2 * ((G::P + 1) / 2);
+#pragma unroll
+      for (int k = 0; k < G::NE; ++k) sh.vu[k] = word_to_f12(w[VB + k], one) - 0.99999994039535522f;
+    }
+  }
+  const float u = utility_of_b<N, EST, MODEL>(b, sh, pr);
   if constexpr (DBG) {
 #pragma unroll
     for (int k = 0; k < G::NNORM; ++k) dbg[k] = nrm[k] * BM_K;

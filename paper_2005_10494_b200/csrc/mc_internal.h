@@ -60,6 +60,9 @@ struct mc_ctx {
   int n = 0;
   int est = 0;
   int model = 0;                         // 0 Gaussian prior (Formula 10 / general), 1 C4 strata prior
+  int sampling = 0;                      // 0 independent draws per design, 1 common random numbers (f3)
+  int32_t* d_crn = nullptr;              // CRN design blocks (first, count, problem) for [crn_d0, +crn_dc)
+  int64_t crn_blocks = 0, crn_d0 = -1, crn_dc = -1;
   int32_t n_probs = 0;
   int64_t D = 0;
   uint64_t seed = 0;

@@ -11,6 +11,8 @@
 #include <cfloat>
 #include <math_constants.h>
 #include <cstdint>
+#include <vector>
+#include <algorithm>
 
 #include "mc_device.cuh"
 #include "mc_internal.h"
@@ -79,7 +81,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
       for (int st = 0; st < STEPS; ++st) {
         uint32_t w[G::BLOCKS * 4];
 #pragma unroll
-        for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk, &w[4 * b]);
+        for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk.k1[0], rk, &w[4 * b]);
         ql += G::BLOCKS;
 #pragma unroll
         for (int l = 0; l < G::L; ++l)
@@ -158,6 +160,163 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// NEXT f3: common random numbers.  The stream is keyed (problem, sample) with tag 1 (counter
+// (q_lo, q_hi, problem, 1)); every design of the problem sees the same draws, so the design-
+// independent part of a draw (Philox, Box-Muller, the prior term, the IND null vector, the SOV
+// uniforms) is computed once and reused for a block of CRN_KD designs held in registers.
+constexpr int CRN_KD = 8;
+
+template <int N, int EST, int MODEL, bool MASKED>
+__device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64_t E, uint32_t pid, const RoundKeys& rk,
+                                            const float (&zc)[CRN_KD][N], const ProbRegs<N>& pr, const StrataRegs& sr,
+                                            uint32_t (&a1)[CRN_KD], uint32_t (&a2)[CRN_KD]) {
+  using G = Geo<N, EST, MODEL>;
+  constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
+  const uint32_t one = one_bits_reg();
+  const uint32_t lo1d = 0xCD9E8D57u * pid, hi1d = __umulhi(0xCD9E8D57u, pid);
+  uint64_t q = s_begin * (uint64_t)G::U / 4;
+  const uint32_t k1r1 = rk.k1[0] ^ 1u;   // counter word 3 = tag 1
+#pragma unroll 1
+  for (int st = 0; st < STEPS; ++st) {
+    const uint64_t s0 = s_begin + (uint64_t)st * G::L;
+    if (MASKED && s0 >= E) break;
+    uint32_t w[G::BLOCKS * 4];
+#pragma unroll
+    for (int b = 0; b < G::BLOCKS; ++b) {
+      const uint64_t qb = q + b;
+      philox_block_lo((uint32_t)qb, hi1d ^ (uint32_t)(qb >> 32) ^ rk.k0[0], lo1d, k1r1, rk, &w[4 * b]);
+    }
+    q += G::BLOCKS;
+#pragma unroll
+    for (int l = 0; l < G::L; ++l) {
+      Shared<N, EST, MODEL> sh;
+      draw_shared<N, EST, MODEL>(&w[l * G::U], one, pr, &sr, sh);
+      bool valid = true;
+      if (MASKED) {
+        const uint64_t s = s0 + l;
+        valid = s >= B && s < E;
+      }
+#pragma unroll
+      for (int k = 0; k < CRN_KD; ++k) {
+        float b[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) b[i] = zc[k][i] - sh.v[i];
+        float u = utility_of_b<N, EST, MODEL>(b, sh, pr);
+        if (MASKED) u = valid ? u : 0.0f;
+        accumulate<EST>(u, a1[k], a2[k]);
+      }
+    }
+  }
+  if constexpr (EST == 1)
+#pragma unroll
+    for (int k = 0; k < CRN_KD; ++k) a2[k] = a1[k];
+}
+
+// Work unit = warp tile (design block of <= CRN_KD designs of one problem, 32 x SAMPLES_PER_THREAD samples).
+template <int N, int EST, int MODEL>
+__global__ void __launch_bounds__(MAX_BLOCK, 2) mc_crn_kernel(
+    const float* __restrict__ prob, const float* __restrict__ zc_all, const int32_t* __restrict__ blk_first,
+    const int32_t* __restrict__ blk_count, const int32_t* __restrict__ blk_prob, uint64_t B, uint64_t E,
+    uint64_t Balign, int64_t tiles_per_block, int64_t total_tiles, const RoundKeys rk,
+    unsigned long long* __restrict__ sums) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  constexpr uint64_t tile_samples = 32ull * SAMPLES_PER_THREAD;
+  for (int64_t tile = gw; tile < total_tiles; tile += nw) {
+    const int64_t j = tile / tiles_per_block;
+    const int64_t chunk = tile % tiles_per_block;
+    const int p = __ldg(blk_prob + j);
+    const int64_t d0 = __ldg(blk_first + j);
+    const int cnt = __ldg(blk_count + j);
+    const float* rec = prob + (int64_t)p * PROB_STRIDE;
+    ProbRegs<N> pr;
+    load_problem<N>(rec, pr);
+    StrataRegs sr;
+    if constexpr (MODEL == 1) load_strata(rec, sr);
+    float zc[CRN_KD][N];
+#pragma unroll
+    for (int k = 0; k < CRN_KD; ++k)
+#pragma unroll
+      for (int i = 0; i < N; ++i) zc[k][i] = k < cnt ? __ldg(zc_all + (d0 + k) * N + i) : __int_as_float(0x7f800000);
+    const uint64_t s_begin = Balign + (uint64_t)chunk * tile_samples + (uint64_t)lane * SAMPLES_PER_THREAD;
+    uint32_t a1[CRN_KD], a2[CRN_KD];
+#pragma unroll
+    for (int k = 0; k < CRN_KD; ++k) a1[k] = a2[k] = 0u;
+    if (s_begin >= B && s_begin + SAMPLES_PER_THREAD <= E)
+      crn_samples<N, EST, MODEL, false>(s_begin, B, E, (uint32_t)p, rk, zc, pr, sr, a1, a2);
+    else if (s_begin < E)
+      crn_samples<N, EST, MODEL, true>(s_begin, B, E, (uint32_t)p, rk, zc, pr, sr, a1, a2);
+#pragma unroll
+    for (int k = 0; k < CRN_KD; ++k) {
+      unsigned long long v1 = a1[k], v2 = a2[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      if (lane == 0 && k < cnt) {
+        atomicAdd(sums + 2 * (d0 + k), v1);
+        atomicAdd(sums + 2 * (d0 + k) + 1, v2);
+      }
+    }
+  }
+}
+
+template <int N, int EST, int MODEL = 0>
+static cudaError_t launch_crn_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
+                                int64_t* sums) {
+  using G = Geo<N, EST, MODEL>;
+  // design blocks of <= CRN_KD consecutive designs that never straddle a problem (cached per range)
+  if (c->crn_d0 != d0 || c->crn_dc != dcount || !c->d_crn) {
+    std::vector<int32_t> first, count, pb;
+    for (int k = 0; k < c->n_probs; ++k) {
+      const int64_t b = std::max<int64_t>(c->prob_begin[k], d0), e = std::min<int64_t>(c->prob_begin[k + 1], d0 + dcount);
+      for (int64_t x = b; x < e; x += CRN_KD) {
+        first.push_back((int32_t)x);
+        count.push_back((int32_t)std::min<int64_t>(CRN_KD, e - x));
+        pb.push_back(k);
+      }
+    }
+    cudaFree(c->d_crn);
+    c->d_crn = nullptr;
+    c->crn_blocks = (int64_t)first.size();
+    if (c->crn_blocks == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&c->d_crn, sizeof(int32_t) * 3 * c->crn_blocks);
+    if (e != cudaSuccess) return e;
+    std::vector<int32_t> all(first);
+    all.insert(all.end(), count.begin(), count.end());
+    all.insert(all.end(), pb.begin(), pb.end());
+    e = cudaMemcpy(c->d_crn, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    c->crn_d0 = d0;
+    c->crn_dc = dcount;
+  }
+  const int threads = c->block_threads;
+  const uint64_t tile = 32ull * SAMPLES_PER_THREAD;
+  const uint64_t Balign = B - (B % G::L);
+  const int64_t tpb = (int64_t)((E - Balign + tile - 1) / tile);
+  const int64_t total = tpb * c->crn_blocks;
+  int grid = c->grid_blocks;
+  if (grid <= 0) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mc_crn_kernel<N, EST, MODEL>, threads, 0);
+    grid = nsm * (per > 0 ? per : 1);
+  }
+  const int64_t wpb = threads / 32;
+  if ((int64_t)grid * wpb > total) grid = (int)((total + wpb - 1) / wpb);
+  if (grid <= 0) return cudaSuccess;
+  const int32_t* bf = c->d_crn;
+  mc_crn_kernel<N, EST, MODEL><<<grid, threads, 0, st>>>(c->d_prob, c->d_zc, bf, bf + c->crn_blocks,
+                                                         bf + 2 * c->crn_blocks, B, E, Balign, tpb, total,
+                                                         round_keys(c->seed), reinterpret_cast<unsigned long long*>(sums));
+  c->launches += 1;
+  return cudaGetLastError();
+}
+
 template <int N, int EST, int MODEL = 0>
 static cudaError_t launch_fused_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
                                   int64_t* sums) {
@@ -204,6 +363,15 @@ template <int EST>
 static mc_status launch_fused_est(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
                                   int64_t* sums) {
   cudaError_t e = cudaSuccess;
+  if (c->sampling == 1) {
+    if (c->model == 1) e = launch_crn_t<2, EST, 1>(c, d0, dcount, B, E, st, sums);
+    else if (c->n == 1) e = launch_crn_t<1, EST>(c, d0, dcount, B, E, st, sums);
+    else if (c->n == 2) e = launch_crn_t<2, EST>(c, d0, dcount, B, E, st, sums);
+    else if (c->n == 3) e = launch_crn_t<3, EST>(c, d0, dcount, B, E, st, sums);
+    else { set_error("common random numbers are built for n <= 3"); return MC_ERR_INVALID; }
+    if (e != cudaSuccess) return cuda_fail(e, "mc_crn_kernel launch");
+    return MC_OK;
+  }
   if (c->model == 1) {
     e = launch_fused_t<2, EST, 1>(c, d0, dcount, B, E, st, sums);
     if (e != cudaSuccess) return cuda_fail(e, "mc_fused_kernel launch");
@@ -293,7 +461,7 @@ mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64
 }
 
 // Per-draw dump through the fused kernel's draw_utility (test hook).
-template <int N, int EST, int MODEL>
+template <int N, int EST, int MODEL, bool CRN>
 __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restrict__ zc_all,
                             const int32_t* __restrict__ pod, uint64_t seed, const int64_t* __restrict__ design,
                             const uint64_t* __restrict__ sample, int64_t count, float* __restrict__ out) {
@@ -309,7 +477,8 @@ __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restr
   for (int k = 0; k < N; ++k) zc[k] = zc_all[d * N + k];
   uint32_t w[G::U];
   const uint64_t base = sample[i] * (uint64_t)G::U;
-  for (int k = 0; k < G::U; ++k) w[k] = philox_word(seed, (uint32_t)d, base + k);
+  for (int k = 0; k < G::U; ++k)
+    w[k] = CRN ? philox_word_tagged(seed, (uint32_t)pod[d], 1u, base + k) : philox_word(seed, (uint32_t)d, base + k);
   float bsc[N];
   for (int k = 0; k < N; ++k) bsc[k] = prob[(int64_t)pod[d] * PROB_STRIDE + OFF_BSC + k];
   draw_utility<N, EST, true, MODEL>(w, 0x3F800000u, zc, pr, out + i * G::DUMP, bsc, &sr);
@@ -318,8 +487,12 @@ __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restr
 template <int N, int EST, int MODEL = 0>
 static cudaError_t launch_dump_t(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
                                  cudaStream_t st) {
-  k_draw_dump<N, EST, MODEL><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod, c->seed,
-                                                                             design, sample, count, out);
+  if (c->sampling == 1)
+    k_draw_dump<N, EST, MODEL, true><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod,
+                                                                                   c->seed, design, sample, count, out);
+  else
+    k_draw_dump<N, EST, MODEL, false><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod,
+                                                                                    c->seed, design, sample, count, out);
   return cudaGetLastError();
 }
 

@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
         L.mc_design_init.restype = i32
         L.mc_design_upload.argtypes = [vp, P(d), vp]; L.mc_design_upload.restype = i32
         L.mc_set_launch.argtypes = [vp, i32, i32]; L.mc_set_launch.restype = i32
+        L.mc_set_sampling.argtypes = [vp, i32]; L.mc_set_sampling.restype = i32
         L.mc_destroy.argtypes = [vp]; L.mc_destroy.restype = None
         L.mc_evaluate_grid.argtypes = [vp, i64, i64, u64, u64, vp, vp]; L.mc_evaluate_grid.restype = i32
         L.mc_finalize.argtypes = [vp, vp, u64, vp, vp, vp]; L.mc_finalize.restype = i32
@@ -91,7 +92,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer", "mc_candidates",
-            "mc_design_init", "mc_design_upload", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
+            "mc_design_init", "mc_design_upload", "mc_set_sampling", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
             "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
 
@@ -264,6 +265,10 @@ class Design:
             alpha_host = np.ascontiguousarray(alpha_host, dtype=np.float64)
             ptr = _dp(alpha_host)
         _check(lib().mc_design_upload(self._ctx, ptr, _stream(stream)))
+
+    def set_sampling(self, crn: bool):
+        """NEXT f3: common random numbers per problem (True) or independent draws per design."""
+        _check(lib().mc_set_sampling(self._ctx, 1 if crn else 0))
 
     def set_launch(self, block_threads: int = 0, grid_blocks: int = 0):
         _check(lib().mc_set_launch(self._ctx, block_threads, grid_blocks))

@@ -334,3 +334,71 @@ def test_c4_strata_prior_parity(O, mc, torch, est):
         assert np.allclose(rec[i, nn:nn + 2], o["b"], atol=2e-4 * (1 + np.abs(o["b"]).max()))
         if est == 0:
             assert abs(rec[i, -1] - o["u"]) <= 1e-4
+
+
+@pytest.mark.parametrize("est", [0, 1])
+def test_crn_parity_and_invariance(O, mc, torch, est):
+    """NEXT f3 common random numbers: the stream is keyed (problem, sample) with tag 1; every design of a
+    problem must equal the oracle's CRN sums, and the sums are invariant to launch shape and splits."""
+    specs = [W.c2_slice(), W.ProblemSpec(r=(1.0, 0.7, 0.2), scenario="b", i3=211.0)]
+    alpha, pod = [], []
+    for k, sp in enumerate(specs):
+        _, a = slice_designs(O, m=16, count=11, seed=20 + k) if k == 0 else (None, None)
+        if k == 1:
+            rows = []
+            for a1, a2 in [(0.002, 0.01), (0.01, 0.002), (0.006, 0.006), (0.012, 0.004)]:
+                a3 = O.solve_alpha_n(sp.r, sp.alpha0, [a1, a2], 1e-13)
+                if a3 is not None:
+                    rows.append([a1, a2, a3])
+            a = np.array(rows)
+        alpha.append(a)
+        pod += [k] * len(a)
+    alpha = np.concatenate(alpha)
+    pod = np.array(pod, dtype=np.int32)
+    dsg = mc.Design([lib_problem(mc, s) for s in specs], alpha, pod, seed=SEED, estimator=est)
+    dsg.set_sampling(True)
+    N = 20_000
+    ref_s = dsg.new_sums()
+    dsg.evaluate(ref_s, 0, N)
+    got = dsg.finalize(ref_s, N)[0].cpu().numpy()
+    flips = 0
+    for d in range(len(alpha)):
+        op = oracle_problem(O, specs[pod[d]])
+        o = O.design_sums(op, alpha[d], est, SEED, int(pod[d]), 0, N, tag=1)
+        if est == 0:
+            ref = O.finalize(o, N)[0][0]
+            assert abs(got[d] - ref) <= REL * ref, (d, got[d], ref)
+        else:
+            flips += abs(int(ref_s[d, 0].item()) - int(o[0])) // 2**23
+    assert flips <= 2
+    for threads, grid in [(64, 5), (256, 1)]:
+        dsg.set_launch(threads, grid)
+        s2 = dsg.new_sums()
+        dsg.evaluate(s2, 0, 7_001)
+        dsg.evaluate(s2, 7_001, N - 7_001)
+        assert torch.equal(s2, ref_s)
+    dsg.set_launch(0, 0)
+    # per-draw records come from the problem's stream
+    D = torch.tensor([0, 3, len(alpha) - 1] * 8).cuda()
+    S = torch.arange(24).cuda() * 977
+    rec = dsg.draw_dump(D, S).cpu().numpy()
+    for i in range(24):
+        d = int(D[i])
+        o = O.draw(oracle_problem(O, specs[pod[d]]), alpha[d], est, SEED, int(pod[d]), int(S[i]), tag=1)
+        if est == 0:
+            assert abs(rec[i, -1] - o["u"]) <= 5e-5
+        else:
+            assert rec[i, -1] == o["u"] or np.min(np.abs(o["xnull"] - o["b"])) < 1e-4
+
+
+def test_crn_ind_is_pathwise_monotone(O, mc, torch):
+    """Under CRN every design sees the same (Delta, X) per sample, so a design whose alphas dominate
+    another's rejects on a superset of samples: its integer count is >= (exactly, not statistically)."""
+    spec = W.c2_slice()
+    alpha = np.array([[0.002, 0.010, 0.010], [0.003, 0.011, 0.012], [0.002, 0.010, 0.0]])
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(3, dtype=np.int32), seed=SEED, estimator=1)
+    dsg.set_sampling(True)
+    s = dsg.new_sums()
+    dsg.evaluate(s, 0, 200_000)
+    S = s.cpu().numpy()[:, 0]
+    assert S[1] >= S[0] >= S[2]

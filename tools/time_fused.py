@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--draws", type=int, default=1_000_000)
+    ap.add_argument("--crn", action="store_true")
     a = ap.parse_args()
     import torch
     from paper_2005_10494_b200 import mc
@@ -28,6 +29,8 @@ def main():
     alpha, pod = mc.candidates(probs, m=W.GRID_M, n3=W.N3, seed=W.SEED)
     dsg = mc.Design(probs, alpha, pod, seed=W.SEED, estimator=0 if a.est == "cond" else 1)
     dsg.set_launch(a.threads, a.grid)
+    if a.crn:
+        dsg.set_sampling(True)
     sums = dsg.new_sums()
     for _ in range(2):
         dsg.evaluate(sums, 0, a.draws)
@@ -39,7 +42,7 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
-    print(json.dumps({"lib": mc.lib_path(), "est": a.est, "threads": a.threads, "designs": dsg.D,
+    print(json.dumps({"lib": mc.lib_path(), "est": a.est, "crn": a.crn, "threads": a.threads, "designs": dsg.D,
                       "ms": ms, "draws_per_s": dsg.D * a.draws / (ms * 1e-3)}), flush=True)
 
 
