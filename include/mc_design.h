@@ -153,6 +153,19 @@ mc_status mc_evaluate_grid(mc_ctx* ctx, int64_t design_begin, int64_t design_cou
                            uint64_t sample_begin, uint64_t sample_count, void* cuda_stream,
                            int64_t* sums_dev);
 
+/* NEXT f3 (ii): the paper-literal CROSSED estimator of Formula 7 (reading R1 alternative).
+ * Per design d: N1 outer prior draws Delta^(k) (stream (d, tag 2), 2ceil(n/2) words per draw) crossed
+ * with N2 inner null draws x^(l) (stream (d, tag 3), 2ceil(n/2) words per draw) — all N1 N2 pairs.
+ * ACCUMULATES the exact integers S1 = sum_k c_k and S2 = sum_k c_k^2 into sums_dev[D*2], with
+ * c_k = #{l : exists i x_i^(l) > b_i^(k)}.  The ctx must be built with MC_EST_IND and a Gaussian prior;
+ * n <= 4; N2 < 2^32.  Asynchronous. */
+mc_status mc_evaluate_crossed(mc_ctx* ctx, uint64_t n1, uint64_t n2, void* cuda_stream, int64_t* sums_dev);
+
+/* Crossed finalize: mean_d = S1/(N1 N2); var_d = sample variance over k of c_k/N2 (the outer-draw
+ * variance that governs the crossed estimator: SE = sqrt(var/N1)).  Asynchronous. */
+mc_status mc_finalize_crossed(mc_ctx* ctx, const int64_t* sums_dev, uint64_t n1, uint64_t n2, double* mean_dev,
+                              double* var_dev, void* cuda_stream);
+
 /* ---- a8: finalize ----------------------------------------------------------------------- */
 
 /* mean_d = S1/(N 2^23); var_d = (S2/(N 2^23) - mean_d^2) N/(N-1) (per-draw variance, A.2),

@@ -512,3 +512,46 @@ void or_subset(int64_t V, int64_t n3, uint64_t seed, int64_t *out)
     qsort(out, (size_t)n3, sizeof(int64_t), cmp_i64);
     free(idx);
 }
+
+/* NEXT f3 (ii): Formula 7 literally: every outer prior draw Delta^(k) (stream (design, tag 2),
+ * 2ceil(p/2) words per draw) paired with every inner null draw x^(l) (stream (design, tag 3),
+ * 2ceil(n/2) words per draw).  sums += (sum_k c_k, sum_k c_k^2), c_k = #{l : exists i x_i^(l) > b_i^(k)}. */
+void or_design_sums_crossed(int n, const double *r, double i3, const double *theta, const double *Lp,
+                            const double *z, uint64_t seed, uint32_t design, uint64_t n1, uint64_t n2, int64_t *sums)
+{
+    const int p = n, uo = 2 * ((p + 1) / 2), ui = 2 * ((n + 1) / 2);
+    double S0[OR_MAXN * OR_MAXN], L0[OR_MAXN * OR_MAXN];
+    or_null_corr(n, r, S0);
+    if (or_cholesky(n, S0, L0) != 0) return;
+    double *X = (double *)malloc(sizeof(double) * (size_t)(n2 > 0 ? n2 : 1) * n);
+    for (uint64_t l = 0; l < n2; ++l) {
+        double w[2 * OR_MAXN + 2];
+        bm_normals(seed, design, 3u, l * (uint64_t)ui, n, w);
+        for (int i = 0; i < n; ++i) {
+            double x = 0.0;
+            for (int k = 0; k <= i; ++k) x += L0[i * n + k] * w[k];
+            X[l * n + i] = x;
+        }
+    }
+    int64_t s1 = 0, s2 = 0;
+    for (uint64_t k = 0; k < n1; ++k) {
+        double eps[2 * OR_MAXN + 2], b[OR_MAXN];
+        bm_normals(seed, design, 2u, k * (uint64_t)uo, p, eps);
+        for (int i = 0; i < n; ++i) {
+            double dl = theta[i];
+            for (int c = 0; c <= i; ++c) dl += Lp[i * p + c] * eps[c];
+            b[i] = z[i] - sqrt(r[i] * i3) * dl;
+        }
+        int64_t ck = 0;
+        for (uint64_t l = 0; l < n2; ++l) {
+            int rej = 0;
+            for (int i = 0; i < n; ++i) if (X[l * n + i] > b[i]) rej = 1;
+            ck += rej;
+        }
+        s1 += ck;
+        s2 += ck * ck;
+    }
+    free(X);
+    sums[0] += s1;
+    sums[1] += s2;
+}

@@ -65,6 +65,7 @@ def lib():
         L.or_alpha_grid.argtypes = [i32, P(d), d, i32, d, P(d), P(ctypes.c_uint8)]
         L.or_alpha_grid.restype = i64
         L.or_subset.argtypes = [i64, i64, u64, P(i64)]
+        L.or_design_sums_crossed.argtypes = [i32, P(d), d, P(d), P(d), P(d), u64, u32, u64, u64, P(i64)]
         L.or_draw_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u32, u64, P(d), P(d), P(d), P(d)]
         L.or_draw_strata.restype = d
         L.or_design_sums_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u32, u64, u64, P(i64)]
@@ -512,3 +513,21 @@ def refine(sites, y, lam: float = -1.0):
     res = minimize(lambda x: tuple(-v for v in tps_eval(sites, w, beta, x)), x0, jac=True, method="L-BFGS-B",
                    bounds=bounds, options={"ftol": 1e-15, "gtol": 1e-12, "maxiter": 500, "maxcor": 10})
     return res.x, -float(res.fun), lam
+
+
+# --------------------------------------------------------------------------------------
+# NEXT f3 (ii): the crossed N1 x N2 estimator of Formula 7
+
+def design_sums_crossed(prob: Problem, alpha, seed: int, design: int, n1: int, n2: int) -> np.ndarray:
+    z = thresholds(alpha)
+    sums = np.zeros(2, dtype=np.int64)
+    lib().or_design_sums_crossed(prob.n, _dp(prob.r), prob.i3, _dp(prob.theta), _dp(prob.Lp), _dp(z), seed, design,
+                                 n1, n2, sums.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    return sums
+
+
+def finalize_crossed(sums, n1: int, n2: int):
+    S = np.asarray(sums, dtype=np.float64).reshape(-1, 2)
+    mean = S[:, 0] / (n1 * n2)
+    var = (S[:, 1] / (n2 * n2) - n1 * mean * mean) / max(n1 - 1, 1)
+    return mean, var

@@ -63,6 +63,7 @@ struct mc_ctx {
   int sampling = 0;                      // 0 independent draws per design, 1 common random numbers (f3)
   int32_t* d_crn = nullptr;              // CRN design blocks (first, count, problem) for [crn_d0, +crn_dc)
   int64_t crn_blocks = 0, crn_d0 = -1, crn_dc = -1;
+  int crn_kd = 0;
   int32_t n_probs = 0;
   int64_t D = 0;
   uint64_t seed = 0;

@@ -165,12 +165,26 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused
 // (q_lo, q_hi, problem, 1)); every design of the problem sees the same draws, so the design-
 // independent part of a draw (Philox, Box-Muller, the prior term, the IND null vector, the SOV
 // uniforms) is computed once and reused for a block of CRN_KD designs held in registers.
-constexpr int CRN_KD = 8;
+// designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 4 / 2,
+// IND 16 / 4
+#ifndef MC_CRN_KD_COND
+#define MC_CRN_KD_COND 4
+#endif
+#ifndef MC_CRN_KD_IND
+#define MC_CRN_KD_IND 16
+#endif
+#ifndef MC_CRN_MINB_COND
+#define MC_CRN_MINB_COND 2
+#endif
+#ifndef MC_CRN_MINB_IND
+#define MC_CRN_MINB_IND 4
+#endif
+template <int EST> constexpr int crn_kd() { return EST == 0 ? MC_CRN_KD_COND : MC_CRN_KD_IND; }
 
-template <int N, int EST, int MODEL, bool MASKED>
+template <int N, int EST, int MODEL, bool MASKED, int KD>
 __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64_t E, uint32_t pid, const RoundKeys& rk,
-                                            const float (&zc)[CRN_KD][N], const ProbRegs<N>& pr, const StrataRegs& sr,
-                                            uint32_t (&a1)[CRN_KD], uint32_t (&a2)[CRN_KD]) {
+                                            const float (&zc)[KD][N], const ProbRegs<N>& pr, const StrataRegs& sr,
+                                            uint32_t (&a1)[KD], uint32_t (&a2)[KD]) {
   using G = Geo<N, EST, MODEL>;
   constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
   const uint32_t one = one_bits_reg();
@@ -198,7 +212,7 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
         valid = s >= B && s < E;
       }
 #pragma unroll
-      for (int k = 0; k < CRN_KD; ++k) {
+      for (int k = 0; k < KD; ++k) {
         float b[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) b[i] = zc[k][i] - sh.v[i];
@@ -210,12 +224,12 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
   }
   if constexpr (EST == 1)
 #pragma unroll
-    for (int k = 0; k < CRN_KD; ++k) a2[k] = a1[k];
+    for (int k = 0; k < KD; ++k) a2[k] = a1[k];
 }
 
-// Work unit = warp tile (design block of <= CRN_KD designs of one problem, 32 x SAMPLES_PER_THREAD samples).
+// Work unit = warp tile (design block of <= KD designs of one problem, 32 x SAMPLES_PER_THREAD samples).
 template <int N, int EST, int MODEL>
-__global__ void __launch_bounds__(MAX_BLOCK, 2) mc_crn_kernel(
+__global__ void __launch_bounds__(MAX_BLOCK, EST == 0 ? MC_CRN_MINB_COND : MC_CRN_MINB_IND) mc_crn_kernel(
     const float* __restrict__ prob, const float* __restrict__ zc_all, const int32_t* __restrict__ blk_first,
     const int32_t* __restrict__ blk_count, const int32_t* __restrict__ blk_prob, uint64_t B, uint64_t E,
     uint64_t Balign, int64_t tiles_per_block, int64_t total_tiles, const RoundKeys rk,
@@ -235,21 +249,22 @@ __global__ void __launch_bounds__(MAX_BLOCK, 2) mc_crn_kernel(
     load_problem<N>(rec, pr);
     StrataRegs sr;
     if constexpr (MODEL == 1) load_strata(rec, sr);
-    float zc[CRN_KD][N];
+    constexpr int KD = crn_kd<EST>();
+    float zc[KD][N];
 #pragma unroll
-    for (int k = 0; k < CRN_KD; ++k)
+    for (int k = 0; k < KD; ++k)
 #pragma unroll
       for (int i = 0; i < N; ++i) zc[k][i] = k < cnt ? __ldg(zc_all + (d0 + k) * N + i) : __int_as_float(0x7f800000);
     const uint64_t s_begin = Balign + (uint64_t)chunk * tile_samples + (uint64_t)lane * SAMPLES_PER_THREAD;
-    uint32_t a1[CRN_KD], a2[CRN_KD];
+    uint32_t a1[KD], a2[KD];
 #pragma unroll
-    for (int k = 0; k < CRN_KD; ++k) a1[k] = a2[k] = 0u;
+    for (int k = 0; k < KD; ++k) a1[k] = a2[k] = 0u;
     if (s_begin >= B && s_begin + SAMPLES_PER_THREAD <= E)
-      crn_samples<N, EST, MODEL, false>(s_begin, B, E, (uint32_t)p, rk, zc, pr, sr, a1, a2);
+      crn_samples<N, EST, MODEL, false, KD>(s_begin, B, E, (uint32_t)p, rk, zc, pr, sr, a1, a2);
     else if (s_begin < E)
-      crn_samples<N, EST, MODEL, true>(s_begin, B, E, (uint32_t)p, rk, zc, pr, sr, a1, a2);
+      crn_samples<N, EST, MODEL, true, KD>(s_begin, B, E, (uint32_t)p, rk, zc, pr, sr, a1, a2);
 #pragma unroll
-    for (int k = 0; k < CRN_KD; ++k) {
+    for (int k = 0; k < KD; ++k) {
       unsigned long long v1 = a1[k], v2 = a2[k];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -269,13 +284,14 @@ static cudaError_t launch_crn_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t 
                                 int64_t* sums) {
   using G = Geo<N, EST, MODEL>;
   // design blocks of <= CRN_KD consecutive designs that never straddle a problem (cached per range)
-  if (c->crn_d0 != d0 || c->crn_dc != dcount || !c->d_crn) {
+  constexpr int KD = crn_kd<EST>();
+  if (c->crn_d0 != d0 || c->crn_dc != dcount || c->crn_kd != KD || !c->d_crn) {
     std::vector<int32_t> first, count, pb;
     for (int k = 0; k < c->n_probs; ++k) {
       const int64_t b = std::max<int64_t>(c->prob_begin[k], d0), e = std::min<int64_t>(c->prob_begin[k + 1], d0 + dcount);
-      for (int64_t x = b; x < e; x += CRN_KD) {
+      for (int64_t x = b; x < e; x += KD) {
         first.push_back((int32_t)x);
-        count.push_back((int32_t)std::min<int64_t>(CRN_KD, e - x));
+        count.push_back((int32_t)std::min<int64_t>(KD, e - x));
         pb.push_back(k);
       }
     }
@@ -292,6 +308,7 @@ static cudaError_t launch_crn_t(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t 
     if (e != cudaSuccess) return e;
     c->crn_d0 = d0;
     c->crn_dc = dcount;
+    c->crn_kd = KD;
   }
   const int threads = c->block_threads;
   const uint64_t tile = 32ull * SAMPLES_PER_THREAD;

@@ -69,6 +69,8 @@ def lib() -> ctypes.CDLL:
         L.mc_set_sampling.argtypes = [vp, i32]; L.mc_set_sampling.restype = i32
         L.mc_destroy.argtypes = [vp]; L.mc_destroy.restype = None
         L.mc_evaluate_grid.argtypes = [vp, i64, i64, u64, u64, vp, vp]; L.mc_evaluate_grid.restype = i32
+        L.mc_evaluate_crossed.argtypes = [vp, u64, u64, vp, vp]; L.mc_evaluate_crossed.restype = i32
+        L.mc_finalize_crossed.argtypes = [vp, vp, u64, u64, vp, vp, vp]; L.mc_finalize_crossed.restype = i32
         L.mc_finalize.argtypes = [vp, vp, u64, vp, vp, vp]; L.mc_finalize.restype = i32
         L.mc_smooth_plan.argtypes = [vp, vp, vp]; L.mc_smooth_plan.restype = i32
         L.mc_smooth.argtypes = [vp, vp, d, vp, vp, vp]; L.mc_smooth.restype = i32
@@ -92,7 +94,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer", "mc_candidates",
-            "mc_design_init", "mc_design_upload", "mc_set_sampling", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_finalize", "mc_smooth_plan",
+            "mc_design_init", "mc_design_upload", "mc_set_sampling", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_evaluate_crossed", "mc_finalize_crossed", "mc_finalize", "mc_smooth_plan",
             "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
 
@@ -286,6 +288,19 @@ class Design:
         _check(lib().mc_evaluate_grid(self._ctx, design_begin, design_count, sample_begin, sample_count,
                                       _stream(stream), sums.data_ptr()))
         return sums
+
+    def evaluate_crossed(self, sums, n1: int, n2: int, stream=None):
+        """NEXT f3 (ii): the paper's crossed N1 x N2 estimator (ctx built with EST_IND)."""
+        _check(lib().mc_evaluate_crossed(self._ctx, n1, n2, _stream(stream), sums.data_ptr()))
+        return sums
+
+    def finalize_crossed(self, sums, n1: int, n2: int, stream=None):
+        torch = _torch()
+        mean = torch.empty(self.D, dtype=torch.float64, device=sums.device)
+        var = torch.empty(self.D, dtype=torch.float64, device=sums.device)
+        _check(lib().mc_finalize_crossed(self._ctx, sums.data_ptr(), n1, n2, mean.data_ptr(), var.data_ptr(),
+                                         _stream(stream)))
+        return mean, var
 
     def finalize(self, sums, total_samples: int, stream=None):
         """Row a8: per-design mean and per-draw variance (fp64 tensors)."""

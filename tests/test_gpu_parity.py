@@ -402,3 +402,26 @@ def test_crn_ind_is_pathwise_monotone(O, mc, torch):
     dsg.evaluate(s, 0, 200_000)
     S = s.cpu().numpy()[:, 0]
     assert S[1] >= S[0] >= S[2]
+
+
+def test_crossed_estimator_parity(O, mc, torch):
+    """NEXT f3 (ii): the paper's crossed N1 x N2 estimator (Formula 7 literally): integer sums equal the
+    oracle's except for pairs decided within fp32 rounding (none expected)."""
+    spec, alpha = slice_designs(O, m=64, count=5, seed=31)
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(len(alpha), dtype=np.int32), seed=SEED, estimator=1)
+    n1, n2 = 1100, 1500          # ragged against the 1024-draw outer block and inner chunk
+    sums = dsg.new_sums()
+    dsg.evaluate_crossed(sums, n1, n2)
+    S = sums.cpu().numpy()
+    op = oracle_problem(O, spec)
+    for d in range(len(alpha)):
+        ref = O.design_sums_crossed(op, alpha[d], SEED, d, n1, n2)
+        assert abs(int(S[d, 0]) - int(ref[0])) <= 3, (d, S[d], ref)
+        if S[d, 0] == ref[0]:
+            assert S[d, 1] == ref[1]
+    mean, var = dsg.finalize_crossed(sums, n1, n2)
+    m_o, v_o = O.finalize_crossed(S, n1, n2)
+    assert np.allclose(mean.cpu().numpy(), m_o, rtol=0, atol=1e-15)
+    with pytest.raises(mc.McError):
+        mc.Design([lib_problem(mc, spec)], alpha, np.zeros(len(alpha), dtype=np.int32), seed=1,
+                  estimator=0).evaluate_crossed(sums, 10, 10)

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--draws", type=int, default=1_000_000)
     ap.add_argument("--crn", action="store_true")
+    ap.add_argument("--crossed", type=str, default="", help="N1,N2: time the crossed estimator (IND ctx)")
     a = ap.parse_args()
     import torch
     from paper_2005_10494_b200 import mc
@@ -32,6 +33,19 @@ def main():
     if a.crn:
         dsg.set_sampling(True)
     sums = dsg.new_sums()
+    if a.crossed:
+        n1, n2 = (int(x) for x in a.crossed.split(","))
+        dsg.evaluate_crossed(sums, n1, n2)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dsg.evaluate_crossed(sums, n1, n2)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        print(json.dumps({"crossed": [n1, n2], "designs": dsg.D, "ms": ms,
+                          "pairs_per_s": dsg.D * n1 * n2 / (ms * 1e-3)}), flush=True)
+        return
     for _ in range(2):
         dsg.evaluate(sums, 0, a.draws)
     torch.cuda.synchronize()
