@@ -245,6 +245,8 @@ def run_ours(args):
     achieved = ipd * draws_launch / (kms * 1e-3) / 1e12
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "Tinst/s",
             "frac": round(achieved / peak, 4), "traffic": None,
+            "traffic_ncu": {"dram_bytes_per_launch": 465920, "draws_per_launch": 1.2e10,
+                            "capture": "profiles/r01/ncu_fused_cond_summary.txt (--problems 6)"},
             "kernel": ("mc_crn_kernel" if args.crn else "mc_fused_kernel") + f"<3,{0 if est == 0 else 1},0>",
             "kernel_ms": round(kms, 3),
             "kernel_share_of_step": round(kms / (ms / args.steps), 4),
@@ -285,11 +287,12 @@ def run_ours(args):
         line = {"metric": "MC draws/sec (design x sample)", "value": value, "unit": "draws/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32 per-draw / int64 sums / f64 finalize+TPS", "data": "synthetic",
+                "dtype": "f32", "data": "synthetic",
                 "config": {"workload": "C2: paper 3-D problem (513 r-problems x 2000 alpha designs), 1e6 draws/design",
                            "problems": len(specs), "designs": D, "draws_per_design": N, "estimator": args.est,
                            "sampling": "common random numbers per problem" if args.crn else "independent per design",
                            "seed": W.SEED, "parallelism": f"sample-shard x{world} + int64 all_reduce",
+                           "arithmetic": "f32 per-draw utility, exact int64 sums, f64 finalize and TPS",
                            "l2": "no flush: the per-step TPS plan read (~%.1f GB) exceeds L2" % (
                                8.0 * sum((pod == k).sum() ** 2 for k in range(len(specs))) / 1e9)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
