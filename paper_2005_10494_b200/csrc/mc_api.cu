@@ -10,8 +10,15 @@
 #include <vector>
 
 #include "mc_internal.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace mci {
+
+// NVTX range for the duration of a C-ABI call (visible in Nsight / ncu --nvtx); header-only NVTX3.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_err;
 
@@ -291,6 +298,7 @@ mc_status mc_problem_strata(double r2, double i3, double alpha0, const double* s
 
 mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs, const double* alpha,
                          const int32_t* pod, int64_t D, uint64_t seed, int32_t estimator, int32_t device) {
+  NvtxRange _nvtx("mc_design_init");
   if (!ctx || !probs || n_probs <= 0 || D < 0 || (D > 0 && (!alpha || !pod))) {
     set_error("mc_design_init: null pointer or empty problem list");
     return MC_ERR_INVALID;
@@ -387,6 +395,7 @@ mc_status mc_design_init(mc_ctx** ctx, const mc_problem* probs, int32_t n_probs,
 }
 
 mc_status mc_design_upload(mc_ctx* c, const double* alpha, void* stream) {
+  NvtxRange _nvtx("mc_design_upload");
   if (!c || (c->D > 0 && !alpha)) { set_error("mc_design_upload: null pointer"); return MC_ERR_INVALID; }
   const int n = c->n;
   for (int64_t d = 0; d < c->D; ++d) {
@@ -447,6 +456,7 @@ void mc_destroy(mc_ctx* c) {
 
 mc_status mc_evaluate_grid(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t s0, uint64_t scount, void* stream,
                            int64_t* sums) {
+  NvtxRange _nvtx("mc_evaluate_grid");
   if (!c || !sums) { set_error("mc_evaluate_grid: null ctx or sums"); return MC_ERR_INVALID; }
   if (d0 < 0 || dcount < 0 || d0 + dcount > c->D) { set_error("mc_evaluate_grid: design range outside [0, D)"); return MC_ERR_INVALID; }
   if (scount > 0 && s0 + scount < s0) { set_error("mc_evaluate_grid: sample range overflows"); return MC_ERR_INVALID; }
@@ -456,6 +466,7 @@ mc_status mc_evaluate_grid(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t s0, u
 }
 
 mc_status mc_finalize(mc_ctx* c, const int64_t* sums, uint64_t N, double* mean, double* var, void* stream) {
+  NvtxRange _nvtx("mc_finalize");
   if (!c || !sums || !mean) { set_error("mc_finalize: null pointer"); return MC_ERR_INVALID; }
   if (N == 0) { set_error("mc_finalize: total_samples must be > 0"); return MC_ERR_INVALID; }
   MC_CUDA(cudaSetDevice(c->device));
@@ -464,6 +475,7 @@ mc_status mc_finalize(mc_ctx* c, const int64_t* sums, uint64_t N, double* mean, 
 
 mc_status mc_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, int64_t* best_idx_host,
                     double* best_val_host, void* stream) {
+  NvtxRange _nvtx("mc_argmax");
   if (!c || !values || !idx || !val) { set_error("mc_argmax: null pointer"); return MC_ERR_INVALID; }
   MC_CUDA(cudaSetDevice(c->device));
   mc_status s = launch_argmax(c, values, idx, val, (cudaStream_t)stream);
@@ -514,6 +526,7 @@ mc_status mc_fwer(const mc_problem* p, const double* alpha, int64_t count, doubl
 
 mc_status mc_candidates(const mc_problem* probs, int32_t n_probs, int32_t m, int64_t n3, uint64_t seed,
                         double* alpha_out, int32_t* problem_out, int64_t cap, int64_t* n_out, int32_t device) {
+  NvtxRange _nvtx("mc_candidates");
   if (!probs || n_probs <= 0 || !n_out || m < 1) { set_error("mc_candidates: null pointer, no problems or m < 1"); return MC_ERR_INVALID; }
   const int n = probs[0].n;
   for (int k = 0; k < n_probs; ++k) {
@@ -590,12 +603,14 @@ mc_status mc_candidates(const mc_problem* probs, int32_t n_probs, int32_t m, int
 }
 
 mc_status mc_smooth_plan(mc_ctx* c, const uint8_t* mask, void* stream) {
+  NvtxRange _nvtx("mc_smooth_plan");
   if (!c) { set_error("mc_smooth_plan: null ctx"); return MC_ERR_INVALID; }
   MC_CUDA(cudaSetDevice(c->device));
   return smooth_plan(c, mask, (cudaStream_t)stream);
 }
 
 mc_status mc_smooth(mc_ctx* c, const double* values, double lambda, double* out, double* lam_used, void* stream) {
+  NvtxRange _nvtx("mc_smooth");
   if (!c || !values || !out) { set_error("mc_smooth: null pointer"); return MC_ERR_INVALID; }
   MC_CUDA(cudaSetDevice(c->device));
   if (!c->plan_built) {

@@ -342,6 +342,38 @@ __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
 #endif
 }
 
+// normal_quantile_fast split for batching: the main polynomial (valid for w < 16) and the deep tail.
+__device__ __forceinline__ float quantile_main(float p, float pc, float& w) {
+  w = -0.69314718056f * (lg2_approx(p * pc) + 2.0f);
+  const float x = sqrt_approx(w + 2.0f) - 2.82842712474619f;
+  float g = -0.0001458914359425521f;
+  g = fmaf(g, x, 0.00014054195626482066f);
+  g = fmaf(g, x, 0.0012376677239334937f);
+  g = fmaf(g, x, -0.0017637622021570974f);
+  g = fmaf(g, x, -0.0036462519812319317f);
+  g = fmaf(g, x, 0.009457966527136036f);
+  g = fmaf(g, x, -0.0013609513949184736f);
+  g = fmaf(g, x, -0.022852510105916587f);
+  g = fmaf(g, x, 0.04599717902636056f);
+  g = fmaf(g, x, -0.040789581299890895f);
+  g = fmaf(g, x, -0.018363709814932894f);
+  g = fmaf(g, x, 1.59782737417905f);
+  g = fmaf(g, x, 3.2334928032079135f);
+  return g * (p - pc);
+}
+__device__ __forceinline__ float quantile_deep(float p, float pc, float w) {
+  constexpr double S2 = 1.4142135623730950488;
+  const float ww = sqrt_approx(fminf(w, 88.0f)) - 6.0f;
+  float g = (float)(7.926354328446905e-07 * S2);
+  g = fmaf(g, ww, (float)(-6.932396900083404e-06 * S2));
+  g = fmaf(g, ww, (float)(2.5214179913746193e-05 * S2));
+  g = fmaf(g, ww, (float)(-3.964155257563107e-05 * S2));
+  g = fmaf(g, ww, (float)(-0.0004801170143764466 * S2));
+  g = fmaf(g, ww, (float)(1.0096029043197632 * S2));
+  g = fmaf(g, ww, (float)(5.859915256500244 * S2));
+  return g * (p - pc);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Per-problem parameters in registers (loaded once per tile; uniform across the block).
 //
@@ -526,6 +558,73 @@ __device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, c
     dbg[G::NNORM + N] = u;
   }
   return u;
+}
+
+// COND with the L draws of a Philox step evaluated stage by stage, so the rare deep-tail inverse-CDF
+// branch is taken once per stage for the whole step instead of once per draw (one large basic block
+// per stage for the scheduler).  Same arithmetic, draw by draw, as draw_utility.
+template <int N, int EST, int MODEL, int L>
+__device__ __forceinline__ void draw_utility_batch(const uint32_t* w, uint32_t one, const float* zc,
+                                                   const ProbRegs<N>& pr, const StrataRegs* sr, float* u) {
+  using G = Geo<N, EST, MODEL>;
+  if constexpr (EST == 1 || MODEL == 1 || G::NE == 0) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) u[l] = draw_utility<N, EST, false, MODEL>(&w[l * G::U], one, zc, pr, nullptr, nullptr, sr);
+  } else {
+    constexpr int VB = 2 * ((G::P + 1) / 2);
+    float b[L][N];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const uint32_t* wl = &w[l * G::U];
+      float nrm[2 * G::NPAIR];
+#pragma unroll
+      for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(wl[2 * j], wl[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        float acc = zc[i];
+#pragma unroll
+        for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
+        b[l][i] = acc;
+      }
+    }
+    float x[L][G::NE];
+#pragma unroll
+    for (int k = 0; k < G::NE; ++k) {
+      float p[L], pc[L], wq[L], y[L];
+      bool deep = false;
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const float a = k == 0 ? b[l][1] : fmaf(-pr.er[k], x[l][k - 1], b[l][2 * k + 1]);
+        float q, e;
+        normal_tail(a, q, e);
+        u[l] = k == 0 ? q : fmaf(1.0f - u[l], q, u[l]);
+        const float v = word_to_f12(w[l * G::U + VB + k], one) - 0.99999994039535522f;
+        p[l] = v * e;
+        pc[l] = fmaf(v, q, 1.0f - v);
+        y[l] = quantile_main(p[l], pc[l], wq[l]);
+        deep = deep || (wq[l] >= 16.0f);
+      }
+      if (deep) {
+#pragma unroll
+        for (int l = 0; l < L; ++l)
+          if (wq[l] >= 16.0f) y[l] = quantile_deep(p[l], pc[l], wq[l]);
+      }
+#pragma unroll
+      for (int l = 0; l < L; ++l) x[l][k] = k == 0 ? y[l] : fmaf(pr.esd[k], y[l], pr.emu[k] * x[l][k - 1]);
+    }
+#pragma unroll
+    for (int j = 0; j < G::NO; ++j) {
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        float a = b[l][2 * j];
+        if (2 * j >= 1) a = fmaf(-pr.oa[j], x[l][j - 1], a);
+        if (2 * j + 1 < N) a = fmaf(-pr.ob[j], x[l][j], a);
+        float q, e;
+        normal_tail(a, q, e);
+        u[l] = fmaf(1.0f - u[l], q, u[l]);
+      }
+    }
+  }
 }
 
 }  // namespace mcd

@@ -83,9 +83,16 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
 #pragma unroll
         for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk.k1[0], rk, &w[4 * b]);
         ql += G::BLOCKS;
+#if MC_BATCH_TAIL
+        float uu[G::L];
+        draw_utility_batch<N, EST, MODEL, G::L>(w, one, zc, pr, &sr, uu);
+#pragma unroll
+        for (int l = 0; l < G::L; ++l) accumulate<EST>(uu[l], a1, a2);
+#else
 #pragma unroll
         for (int l = 0; l < G::L; ++l)
           accumulate<EST>(draw_utility<N, EST, false, MODEL>(&w[l * G::U], one, zc, pr, nullptr, nullptr, &sr), a1, a2);
+#endif
       }
       if constexpr (EST == 1) a2 = a1;
       return;
@@ -167,6 +174,9 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused
 // uniforms) is computed once and reused for a block of CRN_KD designs held in registers.
 // designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 4 / 2,
 // IND 16 / 4
+#ifndef MC_BATCH_TAIL
+#define MC_BATCH_TAIL 0
+#endif
 #ifndef MC_CRN_KD_COND
 #define MC_CRN_KD_COND 4
 #endif

@@ -451,3 +451,20 @@ def evaluate_design_objective(design: Design, total_samples: int, lam: float = -
         sm, lam_used = mean, None
     idx, val, best = design.argmax(sm, stream=stream)
     return Result(mean, var, sm, lam_used, idx, val, best)
+
+
+# ------------------------------------------------------------------------------------------
+# Checkpoint / resume: the integer sums add exactly, so a run is resumed by continuing the
+# sample range from `samples_done` into the saved sums — bit-identical to an uninterrupted run.
+
+def checkpoint_save(path: str, sums, samples_done: int, seed: int, meta: dict = None):
+    import json as _json
+    s = sums.detach().to("cpu").numpy() if hasattr(sums, "detach") else np.asarray(sums)
+    np.savez(path, sums=s.astype(np.int64), samples_done=np.int64(samples_done), seed=np.uint64(seed),
+             meta=np.array(_json.dumps(meta or {})))
+
+
+def checkpoint_load(path: str):
+    import json as _json
+    z = np.load(path if path.endswith(".npz") else path + ".npz")
+    return z["sums"], int(z["samples_done"]), int(z["seed"]), _json.loads(str(z["meta"]))

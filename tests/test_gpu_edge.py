@@ -126,3 +126,18 @@ def test_c2_full_size_sampled_parity(O, mc, torch):
         assert a3 is not None and abs(a3 - alpha[d, 2]) < 1e-11
         ref = O.finalize(O.design_sums(oracle_problem(O, sp), [a12[0], a12[1], a3], 0, SEED, int(d), 0, N), N)[0][0]
         assert abs(mean[d] - ref) <= 1e-5 * ref, (d, mean[d], ref)
+
+
+def test_checkpoint_resume_is_bit_identical(O, mc, torch, tmp_path):
+    spec = W.c2_slice()
+    alpha = np.array([[0.0025, 0.0138, 0.0128], [0.01, 0.005, 0.0123]])
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(2, dtype=np.int32), seed=SEED)
+    full = dsg.new_sums()
+    dsg.evaluate(full, 0, 300_001)
+    part = dsg.new_sums()
+    dsg.evaluate(part, 0, 123_457)
+    mc.checkpoint_save(str(tmp_path / "ck"), part, 123_457, SEED)
+    s, done, seed, _ = mc.checkpoint_load(str(tmp_path / "ck"))
+    resumed = torch.from_numpy(s).cuda()
+    dsg.evaluate(resumed, done, 300_001 - done)
+    assert seed == SEED and torch.equal(resumed, full)

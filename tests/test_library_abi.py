@@ -140,3 +140,10 @@ def test_host_surface_matches_oracle_tps(mc, O):
     y1 = np.sin(3 * x1[:, 0])
     s1 = mc.Surface(x1, y1, 0.0)
     assert np.allclose(s1(x1)[0], y1, atol=1e-10)
+
+
+def test_checkpoint_roundtrip(mc, tmp_path):
+    sums = np.arange(20, dtype=np.int64).reshape(10, 2) * (2**40)
+    mc.checkpoint_save(str(tmp_path / "ck"), sums, 123456789, 0x2005105494, {"designs": 10})
+    s2, done, seed, meta = mc.checkpoint_load(str(tmp_path / "ck"))
+    assert np.array_equal(s2, sums) and done == 123456789 and seed == 0x2005105494 and meta["designs"] == 10
