@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work of the cpu_baseline sample")
+    ap.add_argument("--no-tto-c2", action="store_true", help="skip the C2 time-to-optimal-design bookkeeping")
     ap.add_argument("--tto-draws", type=int, default=W.DRAWS["C3"],
                     help="draws/design of the time-to-optimal-design run (C3 slice); 0 = skip")
     return ap.parse_args()
@@ -173,8 +174,38 @@ def run_ours(args):
         idx, val, _ = design.argmax(sm, with_host=False)
         return idx, val, mean, var
 
-    for _ in range(args.warmup):
-        step()
+    # warm-up step 1 doubles as the end of the C2 time-to-optimal-design run (BASELINE metric 2, the
+    # secondary configuration): problem statement -> candidates -> plan -> one full pass -> the optimum
+    # per problem (f1 L-BFGS on the TPS) -> the TPS over r and its maximum per scenario (f2).
+    tto_c2 = None
+    for wi in range(args.warmup):
+        out_w = step()
+        if wi == 0 and not args.no_tto_c2:
+            _, _, mean_w, _ = out_w
+            A_opt, v_opt, st_opt = design.refine(mean_w, -1.0)
+            per_sc = {}
+            for sc in ("a", "b", "c"):
+                ks = [k for k, sp in enumerate(specs) if sp.scenario == sc and st_opt[k] != 1]
+                if len(ks) < 4:
+                    continue
+                rr = np.array([specs[k].r[1:] for k in ks])
+                surf = mc.Surface(rr, v_opt[ks], -1.0)
+                r_star, p_star = surf.maximum()
+                kbest = ks[int(np.argmax(v_opt[ks]))]
+                per_sc[sc] = {"r_star": [float(x) for x in r_star], "power_r_star": float(p_star),
+                              "best_lattice_r": [float(x) for x in specs[kbest].r[1:]],
+                              "best_lattice_alpha": [float(x) for x in A_opt[kbest]],
+                              "best_lattice_power": float(v_opt[kbest])}
+            torch.cuda.synchronize()
+            tt = torch.tensor([time.perf_counter() - t_prep0], dtype=torch.float64, device=f"cuda:{local}")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tto_c2 = {"seconds": float(tt[0]), "workload": "C2: 513 problems x 2000 designs x 1e6 draws",
+                      "includes": "candidates, thresholds, TPS plans, one MC pass, smoothing, per-problem L-BFGS "
+                                  "optimum, TPS over r per scenario",
+                      "per_scenario": per_sc,
+                      "paper_printed": {"a": "0.6847 at r=(1,0,0)", "b": "0.783 (typo for 0.733, R15) at r2=0.365",
+                                        "c": "0.977 at r=(1,0.446,0.168)"}}
     torch.cuda.synchronize()
     launches0 = design.launches
     clocks = Clocks(local)
@@ -296,7 +327,8 @@ def run_ours(args):
                            "l2": "no flush: the per-step TPS plan read (~%.1f GB) exceeds L2" % (
                                8.0 * sum((pod == k).sum() ** 2 for k in range(len(specs))) / 1e9)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "time_to_optimal_design": tto, "paper_literal_crossed_problem": paper_crossed,
+                "time_to_optimal_design": tto, "time_to_optimal_design_c2": tto_c2,
+                "paper_literal_crossed_problem": paper_crossed,
                 "clocks": clk,
                 "prep_s": {"candidates": round(t_cand, 3), "tps_plan": round(t_plan, 3)},
                 "best_design_first_problem": int(out[0][0].item())}

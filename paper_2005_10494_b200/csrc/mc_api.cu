@@ -438,11 +438,7 @@ mc_status mc_set_launch(mc_ctx* c, int32_t threads, int32_t grid) {
 void mc_destroy(mc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  for (auto& pl : c->plans) {
-    cudaFree(pl.d_fit_idx);
-    cudaFree(pl.d_E);
-    cudaFree(pl.d_lam);
-  }
+  cudaFree(c->d_plan_arena);
   cudaFree(c->d_tps_scratch);
   cudaFree(c->d_crn);
   cudaFree(c->d_prob);

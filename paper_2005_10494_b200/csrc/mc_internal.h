@@ -83,6 +83,7 @@ struct mc_ctx {
   bool plan_built = false;
   std::vector<mci::TpsPlan> plans;
   double* d_tps_scratch = nullptr;       // per-problem scratch for smoothing
+  double* d_plan_arena = nullptr;        // all TPS plans (E, Lambda, fitted indices) in one allocation
   size_t tps_scratch_elems = 0;
   int n_plans = 0;
   // TPS coefficients of the last mc_refine (host): per problem sites, w, beta

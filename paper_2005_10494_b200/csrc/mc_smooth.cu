@@ -14,6 +14,8 @@
 #include <cmath>
 #include <cstring>
 #include <vector>
+#include <thread>
+#include <string>
 
 #include "mc_internal.h"
 
@@ -262,8 +264,17 @@ static void householder_T(const std::vector<double>& X, int64_t N, int d, std::v
     }                                                                                \
   } while (0)
 
-static mc_status build_one(mc_ctx* c, cusolverDnHandle_t h, cudaStream_t st, TpsPlan& pl, const std::vector<int64_t>& fit,
-                           double* d_K, double* d_work, int lwork, int* d_info, double* d_vec) {
+// One lane of the plan builder: its own stream, cuSOLVER handle and scratch (K, workspace, temporaries).
+struct PlanLane {
+  cudaStream_t st = nullptr;
+  cusolverDnHandle_t h = nullptr;
+  double *K = nullptr, *work = nullptr, *X = nullptr, *V = nullptr, *w = nullptr, *p = nullptr, *vec = nullptr;
+  int* info = nullptr;
+  int lwork = 0;
+};
+
+// Plan of one problem into arena slices E (N x (N-k)), lam (N-k), fit_idx (N) on the lane's stream.
+static mc_status build_one(mc_ctx* c, PlanLane& ln, TpsPlan& pl, const std::vector<int64_t>& fit) {
   const int n = c->n, d = n - 1, k = d + 1;
   const int64_t N = (int64_t)fit.size();
   const double a0 = c->probs[c->pod[fit[0]]].alpha0;
@@ -272,64 +283,51 @@ static mc_status build_one(mc_ctx* c, cusolverDnHandle_t h, cudaStream_t st, Tps
     for (int j = 0; j < d; ++j) X[i * d + j] = c->alpha[fit[i] * n + j] / a0;
   std::vector<double> Vh, tau;
   householder_T(X, N, d, Vh, tau);
-  double *d_X = nullptr, *d_V = nullptr, *d_w = nullptr, *d_p = nullptr;
-  MC_CUDA(cudaMalloc(&d_X, sizeof(double) * N * d));
-  MC_CUDA(cudaMalloc(&d_V, sizeof(double) * N * k));
-  MC_CUDA(cudaMalloc(&d_w, sizeof(double) * N));
-  MC_CUDA(cudaMalloc(&d_p, sizeof(double) * N));
-  MC_CUDA(cudaMemcpyAsync(d_X, X.data(), sizeof(double) * N * d, cudaMemcpyHostToDevice, st));
-  MC_CUDA(cudaMemcpyAsync(d_V, Vh.data(), sizeof(double) * N * k, cudaMemcpyHostToDevice, st));
+  cudaStream_t st = ln.st;
+  MC_CUDA(cudaMemcpyAsync(ln.X, X.data(), sizeof(double) * N * d, cudaMemcpyHostToDevice, st));
+  MC_CUDA(cudaMemcpyAsync(ln.V, Vh.data(), sizeof(double) * N * k, cudaMemcpyHostToDevice, st));
+  MC_CUDA(cudaMemcpyAsync(pl.d_fit_idx, fit.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, st));
   const dim3 g2((unsigned)((N + 255) / 256), (unsigned)N);
-  k_tps_kernel_matrix<<<g2, 256, 0, st>>>(d_X, N, d, d_K);
+  k_tps_kernel_matrix<<<g2, 256, 0, st>>>(ln.X, N, d, ln.K);
   // B_full = H_k..H_1 K H_1..H_k
   for (int r = 0; r < k; ++r) {
-    const double* v = d_V + (int64_t)r * N;
-    k_col_dot<<<(unsigned)N, 256, 0, st>>>(d_K, N, N, N, v, d_p);   // A v (A symmetric)
-    k_sym_w<<<1, 1024, 0, st>>>(d_p, v, N, tau[r], d_w);
-    k_rank2<<<g2, 256, 0, st>>>(d_K, N, v, d_w);
+    const double* v = ln.V + (int64_t)r * N;
+    k_col_dot<<<(unsigned)N, 256, 0, st>>>(ln.K, N, N, N, v, ln.p);   // A v (A symmetric)
+    k_sym_w<<<1, 1024, 0, st>>>(ln.p, v, N, tau[r], ln.w);
+    k_rank2<<<g2, 256, 0, st>>>(ln.K, N, v, ln.w);
   }
   MC_CUDA(cudaGetLastError());
   const int64_t m = N - k;
-  double* B = d_K + k + (int64_t)k * N;
-  MC_CUDA(cudaMalloc(&pl.d_lam, sizeof(double) * m));
-  MC_SOLVER(cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)m, B, (int)N, pl.d_lam, d_work,
-                             lwork, d_info));
+  double* B = ln.K + k + (int64_t)k * N;
+  MC_SOLVER(cusolverDnDsyevd(ln.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)m, B, (int)N, pl.d_lam, ln.work,
+                             ln.lwork, ln.info));
+  // E = H_1 .. H_k [0; V]
+  const dim3 g3((unsigned)((N + 255) / 256), (unsigned)m);
+  k_embed<<<g3, 256, 0, st>>>(B, N, k, pl.d_E);
+  for (int r = k - 1; r >= 0; --r) {
+    const double* v = ln.V + (int64_t)r * N;
+    k_col_dot<<<(unsigned)m, 256, 0, st>>>(pl.d_E, N, m, N, v, ln.vec);
+    k_rank1_left<<<g3, 256, 0, st>>>(pl.d_E, N, m, N, v, ln.vec, tau[r]);
+  }
+  MC_CUDA(cudaGetLastError());
   int info = 0;
-  MC_CUDA(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, st));
-  MC_CUDA(cudaStreamSynchronize(st));
+  MC_CUDA(cudaMemcpyAsync(&info, ln.info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MC_CUDA(cudaStreamSynchronize(st));   // host vectors above go out of scope; lane reuse
   if (info != 0) {
     set_error("mc_smooth_plan: Dsyevd failed (info = " + std::to_string(info) + ")");
     return MC_ERR_NUMERIC;
   }
-  // E = H_1 .. H_k [0; V]
-  MC_CUDA(cudaMalloc(&pl.d_E, sizeof(double) * N * m));
-  const dim3 g3((unsigned)((N + 255) / 256), (unsigned)m);
-  k_embed<<<g3, 256, 0, st>>>(B, N, k, pl.d_E);
-  for (int r = k - 1; r >= 0; --r) {
-    const double* v = d_V + (int64_t)r * N;
-    k_col_dot<<<(unsigned)m, 256, 0, st>>>(pl.d_E, N, m, N, v, d_vec);
-    k_rank1_left<<<g3, 256, 0, st>>>(pl.d_E, N, m, N, v, d_vec, tau[r]);
-  }
-  MC_CUDA(cudaGetLastError());
-  MC_CUDA(cudaMalloc(&pl.d_fit_idx, sizeof(int64_t) * N));
-  MC_CUDA(cudaMemcpyAsync(pl.d_fit_idx, fit.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, st));
-  MC_CUDA(cudaStreamSynchronize(st));
-  cudaFree(d_X);
-  cudaFree(d_V);
-  cudaFree(d_w);
-  cudaFree(d_p);
   pl.nfit = N;
   pl.d = d;
   pl.passthrough = false;
   return MC_OK;
 }
 
+constexpr int PLAN_LANES = 8;   // concurrent plan builders (streams + cuSOLVER handles)
+
 mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
-  for (auto& pl : c->plans) {
-    cudaFree(pl.d_fit_idx);
-    cudaFree(pl.d_E);
-    cudaFree(pl.d_lam);
-  }
+  cudaFree(c->d_plan_arena);
+  c->d_plan_arena = nullptr;
   c->plans.assign(c->n_probs, TpsPlan{});
   c->plan_built = false;
   const int d = c->n - 1;
@@ -337,61 +335,88 @@ mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
     set_error("mc_smooth_plan: TPS over more than 3 free alpha coordinates is not supported (n <= 4)");
     return MC_ERR_INVALID;
   }
-  // fitted sets and the largest one (for scratch sizing)
+  MC_CUDA(cudaStreamSynchronize(st));   // the caller's values / alpha are settled
+  // fitted sets, arena layout (E, lam, fit_idx per plan) and the largest set (lane scratch)
   std::vector<std::vector<int64_t>> fits(c->n_probs);
   int64_t Nmax = 0;
+  size_t arena = 0;
+  std::vector<size_t> offE(c->n_probs), offL(c->n_probs), offI(c->n_probs);
+  std::vector<int> todo;
   for (int k = 0; k < c->n_probs; ++k) {
     TpsPlan& pl = c->plans[k];
     pl.begin = c->prob_begin[k];
     pl.count = c->prob_begin[k + 1] - c->prob_begin[k];
     for (int64_t i = pl.begin; i < pl.begin + pl.count; ++i)
       if (!mask || mask[i]) fits[k].push_back(i);
-    if (d >= 1 && (int64_t)fits[k].size() >= d + 2) Nmax = std::max<int64_t>(Nmax, (int64_t)fits[k].size());
+    const int64_t N = (int64_t)fits[k].size();
+    if (d >= 1 && N >= d + 2) {
+      Nmax = std::max<int64_t>(Nmax, N);
+      const int64_t m = N - d - 1;
+      offE[k] = arena; arena += (size_t)N * m;
+      offL[k] = arena; arena += (size_t)m;
+      offI[k] = arena; arena += (size_t)N;    // int64 fits a double slot
+      todo.push_back(k);
+    }
   }
-  if (Nmax > 0) {
-    cusolverDnHandle_t h;
-    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) { set_error("cusolverDnCreate failed"); return MC_ERR_CUDA; }
-    cusolverDnSetStream(h, st);
-    double *d_K = nullptr, *d_work = nullptr, *d_vec = nullptr, *d_lam_tmp = nullptr;
-    int* d_info = nullptr;
-    int lwork = 0;
+  if (!todo.empty()) {
+    MC_CUDA(cudaMalloc(&c->d_plan_arena, sizeof(double) * arena));
+    for (int k : todo) {
+      c->plans[k].d_E = c->d_plan_arena + offE[k];
+      c->plans[k].d_lam = c->d_plan_arena + offL[k];
+      c->plans[k].d_fit_idx = reinterpret_cast<int64_t*>(c->d_plan_arena + offI[k]);
+    }
+    const int nl = std::min<int>(PLAN_LANES, (int)todo.size());
+    std::vector<PlanLane> lanes(nl);
     mc_status s = MC_OK;
-    cudaError_t e;
-    if ((e = cudaMalloc(&d_K, sizeof(double) * Nmax * Nmax)) != cudaSuccess ||
-        (e = cudaMalloc(&d_vec, sizeof(double) * Nmax)) != cudaSuccess ||
-        (e = cudaMalloc(&d_lam_tmp, sizeof(double) * Nmax)) != cudaSuccess ||
-        (e = cudaMalloc(&d_info, sizeof(int))) != cudaSuccess) {
-      s = cuda_fail(e, "mc_smooth_plan alloc");
-    } else {
-      const int m = (int)(Nmax - (d + 1));
-      if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, d_K, (int)Nmax, d_lam_tmp,
-                                      &lwork) != CUSOLVER_STATUS_SUCCESS) {
-        set_error("cusolverDnDsyevd_bufferSize failed");
-        s = MC_ERR_CUDA;
-      } else if ((e = cudaMalloc(&d_work, sizeof(double) * (size_t)lwork)) != cudaSuccess) {
-        s = cuda_fail(e, "mc_smooth_plan workspace");
-      }
-    }
-    for (int k = 0; s == MC_OK && k < c->n_probs; ++k) {
-      if ((int64_t)fits[k].size() < d + 2) continue;
-      // workspace for this size may be smaller than for Nmax: query and grow if needed
+    for (int t = 0; t < nl && s == MC_OK; ++t) {
+      PlanLane& ln = lanes[t];
+      cudaError_t e;
+      if ((e = cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking)) != cudaSuccess) { s = cuda_fail(e, "plan stream"); break; }
+      if (cusolverDnCreate(&ln.h) != CUSOLVER_STATUS_SUCCESS) { set_error("cusolverDnCreate failed"); s = MC_ERR_CUDA; break; }
+      cusolverDnSetStream(ln.h, ln.st);
+      if ((e = cudaMalloc(&ln.K, sizeof(double) * Nmax * Nmax)) != cudaSuccess ||
+          (e = cudaMalloc(&ln.X, sizeof(double) * Nmax * 3)) != cudaSuccess ||
+          (e = cudaMalloc(&ln.V, sizeof(double) * Nmax * 4)) != cudaSuccess ||
+          (e = cudaMalloc(&ln.w, sizeof(double) * Nmax)) != cudaSuccess ||
+          (e = cudaMalloc(&ln.p, sizeof(double) * Nmax)) != cudaSuccess ||
+          (e = cudaMalloc(&ln.vec, sizeof(double) * Nmax)) != cudaSuccess ||
+          (e = cudaMalloc(&ln.info, sizeof(int))) != cudaSuccess) { s = cuda_fail(e, "plan lane alloc"); break; }
+      // workspace for the largest problem (syevd's requirement grows with n)
       int lw = 0;
-      const int64_t N = (int64_t)fits[k].size();
-      cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)(N - d - 1), d_K, (int)N,
-                                  d_lam_tmp, &lw);
-      if (lw > lwork) {
-        cudaFree(d_work);
-        lwork = lw;
-        if ((e = cudaMalloc(&d_work, sizeof(double) * (size_t)lwork)) != cudaSuccess) { s = cuda_fail(e, "workspace"); break; }
+      for (int k : todo) {
+        const int64_t N = (int64_t)fits[k].size();
+        int l = 0;
+        cusolverDnDsyevd_bufferSize(ln.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)(N - d - 1), ln.K, (int)N,
+                                    ln.w, &l);
+        lw = std::max(lw, l);
       }
-      s = build_one(c, h, st, c->plans[k], fits[k], d_K, d_work, lwork, d_info, d_vec);
+      ln.lwork = lw;
+      if ((e = cudaMalloc(&ln.work, sizeof(double) * (size_t)std::max(lw, 1))) != cudaSuccess) { s = cuda_fail(e, "plan workspace"); break; }
     }
-    cudaFree(d_K);
-    cudaFree(d_work);
-    cudaFree(d_vec);
-    cudaFree(d_lam_tmp);
-    cudaFree(d_info);
-    cusolverDnDestroy(h);
+    if (s == MC_OK) {
+      std::vector<mc_status> st_lane(nl, MC_OK);
+      std::vector<std::string> err_lane(nl);
+      auto work = [&](int t) {
+        cudaSetDevice(c->device);
+        for (size_t i = t; i < todo.size(); i += nl) {
+          const int k = todo[i];
+          const mc_status r = build_one(c, lanes[t], c->plans[k], fits[k]);
+          if (r != MC_OK) { st_lane[t] = r; err_lane[t] = mc_last_error(); return; }
+        }
+      };
+      std::vector<std::thread> th;
+      for (int t = 1; t < nl; ++t) th.emplace_back(work, t);
+      work(0);
+      for (auto& x : th) x.join();
+      for (int t = 0; t < nl; ++t)
+        if (st_lane[t] != MC_OK) { s = st_lane[t]; set_error(err_lane[t]); break; }
+    }
+    for (auto& ln : lanes) {
+      if (ln.h) cusolverDnDestroy(ln.h);
+      if (ln.st) cudaStreamDestroy(ln.st);
+      cudaFree(ln.K); cudaFree(ln.work); cudaFree(ln.X); cudaFree(ln.V); cudaFree(ln.w); cudaFree(ln.p);
+      cudaFree(ln.vec); cudaFree(ln.info);
+    }
     if (s != MC_OK) return s;
   }
   // scratch for y and c: sum of fitted sizes
