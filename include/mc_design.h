@@ -132,7 +132,8 @@ mc_status mc_design_upload(mc_ctx* ctx, const double* alpha_host, void* cuda_str
 /* Sampling mode (NEXT f3): 0 = independent draws per design (stream keyed (design, sample), tag 0;
  * the default, reading R2); 1 = common random numbers per problem (stream keyed (problem, sample),
  * counter word 3 = 1): every design of a problem sees the same draws, so design differences have far
- * less noise and the draw's design-independent work is shared by blocks of 8 designs.  n <= 3. */
+ * less noise and the draw's design-independent work is shared by blocks of designs (4 COND, 16 IND).
+ * n <= 3. */
 mc_status mc_set_sampling(mc_ctx* ctx, int32_t mode);
 
 /* Launch shape of the fused kernel (results do not depend on it): threads per block (multiple of
@@ -237,6 +238,9 @@ mc_status mc_argmax(mc_ctx* ctx, const double* values_dev, int64_t* idx_dev, dou
 
 int64_t mc_num_designs(const mc_ctx* ctx);
 int32_t mc_num_problems(const mc_ctx* ctx);
+/* Stream words consumed per sample: IND 2 ceil((p+n)/2); COND p + floor(n/2), since
+ * COND samples come in records of two (2j, 2j+1) sharing p Box-Muller pairs (2p words) followed by
+ * each sample's floor(n/2) SOV uniforms.  -1 for a null ctx. */
 int32_t mc_words_per_draw(const mc_ctx* ctx);
 
 /* K3: Philox words.  out_dev[i] = word word_dev[i] of design design_dev[i]'s stream for `seed`

@@ -181,11 +181,11 @@ void or_null_corr(int n, const double *r, double *S)
  * Returns u in [0,1]: the success probability (COND) or indicator (IND).    */
 int or_words_per_draw(int n, int p, int est)
 {
-    if (est == 0) return 2 * ((p + 1) / 2) + n / 2;
+    if (est == 0) return p + n / 2;     /* a record of 2 samples takes 2p + 2(n/2) words */
     return 2 * ((p + n + 1) / 2);
 }
 
-/* Box-Muller: pair j uses words 2j (radius) and 2j+1 (angle) of the draw. */
+/* Box-Muller: pair j uses words 2j (radius) and 2j+1 (angle) after w0. */
 static void bm_normals(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0, int nnorm, double *normals)
 {
     for (int j = 0; 2 * j < nnorm; ++j) {
@@ -194,6 +194,28 @@ static void bm_normals(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0
         normals[2 * j] = R * cos(a);
         normals[2 * j + 1] = R * sin(a);
     }
+}
+
+/* The normals of sample s and the word index of its first SOV uniform.
+ * COND: samples come in records of two, (2j, 2j+1), of 2p + 2(n/2) words starting at word j(2p + 2(n/2)):
+ * words [0, 2p) are p Box-Muller pairs giving 2p normals, sample 2j takes normals [0, p) and sample
+ * 2j+1 normals [p, 2p); then sample 2j's n/2 uniforms, then sample 2j+1's.
+ * IND: sample s takes words [sU, (s+1)U), U = 2 ceil((p+n)/2): p prior normals then n null normals. */
+static uint64_t sample_normals(int n, int p, int est, uint64_t seed, uint32_t design, uint32_t tag, uint64_t s,
+                               double *normals)
+{
+    if (est == 1) {
+        const uint64_t w0 = s * (uint64_t)or_words_per_draw(n, p, est);
+        bm_normals(seed, design, tag, w0, p + n, normals);
+        return w0 + 2 * ((p + n + 1) / 2);
+    }
+    const uint64_t wr = 2 * (uint64_t)p + 2 * (uint64_t)(n / 2);
+    const uint64_t w0 = (s / 2) * wr;
+    const int h = (int)(s % 2);
+    double rec[4 * OR_MAXN + 4];
+    bm_normals(seed, design, tag, w0, 2 * p, rec);
+    for (int k = 0; k < p; ++k) normals[k] = rec[h * p + k];
+    return w0 + 2 * (uint64_t)p + (uint64_t)h * (n / 2);
 }
 
 /* Utility of one draw given the thresholds b of Phi_Sigma0 (Formulas 4-7):
@@ -259,11 +281,8 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
                const double *z, int est, uint64_t seed, uint32_t design, uint32_t tag, uint64_t s,
                double *eps_out, double *delta_out, double *b_out, double *wnull_out)
 {
-    const int U = or_words_per_draw(n, p, est);
-    const uint64_t w0 = s * (uint64_t)U;
-    const int nnorm = (est == 0) ? p : p + n;
     double normals[2 * OR_MAXN + 2];
-    bm_normals(seed, design, tag, w0, nnorm, normals);
+    const uint64_t vw0 = sample_normals(n, p, est, seed, design, tag, s, normals);
     /* Formula 10: Delta = theta + Lp * eps. */
     double delta[OR_MAXN], b[OR_MAXN];
     for (int i = 0; i < n; ++i) {
@@ -276,7 +295,7 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
     if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
     if (delta_out) for (int i = 0; i < n; ++i) delta_out[i] = delta[i];
     if (b_out) for (int i = 0; i < n; ++i) b_out[i] = b[i];
-    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, w0 + 2 * ((p + 1) / 2), wnull_out);
+    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, vw0, wnull_out);
 }
 
 /* C4 strata prior (a synthetic extension inside the Formula-3 model, not in the paper).
@@ -293,10 +312,8 @@ double or_draw_strata(double r2, double i3, const double *sp, const double *z, i
 {
     const int n = 2, p = 5;
     const double r[2] = { 1.0, r2 };
-    const int U = or_words_per_draw(n, p, est);
-    const uint64_t w0 = s * (uint64_t)U;
     double normals[2 * OR_MAXN + 2];
-    bm_normals(seed, design, tag, w0, est == 0 ? p : p + n, normals);
+    const uint64_t vw0 = sample_normals(n, p, est, seed, design, tag, s, normals);
     const double pi = 1.0 / (1.0 + exp(-(sp[0] + sp[1] * normals[0])));
     const double dp = sp[2] + sp[3] * normals[1];
     const double dm = sp[4] + sp[5] * normals[2];
@@ -314,7 +331,7 @@ double or_draw_strata(double r2, double i3, const double *sp, const double *z, i
     if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
     if (delta_out) { delta_out[0] = d1; delta_out[1] = d2; }
     if (b_out) { b_out[0] = b[0]; b_out[1] = b[1]; }
-    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, w0 + 2 * ((p + 1) / 2), wnull_out);
+    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, vw0, wnull_out);
 }
 
 void or_design_sums_strata(double r2, double i3, const double *sp, const double *z, int est, uint64_t seed,

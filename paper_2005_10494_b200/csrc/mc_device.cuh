@@ -13,20 +13,26 @@ namespace mcd {
 
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
-// Geometry of one draw for N populations, estimator EST (0 COND, 1 IND) and prior MODEL
-// (0: Gaussian, prior dimension P = N; 1: the C4 strata prior, P = 5, N = 2).
+// Geometry of the word stream for N populations, estimator EST (0 COND, 1 IND) and prior MODEL
+// (0: Gaussian, prior dimension P = N; 1: the C4 strata prior, P = 5, N = 2).  The stream of a design
+// is cut into RECORDS of R consecutive samples: COND R = 2 (a sample pair shares P
+// Box-Muller pairs: 2P normals, then NE SOV uniforms per sample), IND R = 1 (NPAIR pairs).
 template <int N, int EST, int MODEL = 0>
 struct Geo {
   static constexpr int P = MODEL == 1 ? 5 : N;
-  static constexpr int NNORM = (EST == 0) ? P : P + N;          // normals per draw
-  static constexpr int NPAIR = (NNORM + 1) / 2;                   // Box-Muller pairs
-  static constexpr int U = (EST == 0) ? 2 * ((P + 1) / 2) + N / 2 : 2 * NPAIR;   // words per draw
+  static constexpr int NNORM = (EST == 0) ? P : P + N;          // normals per sample
   static constexpr int NE = N / 2;           // COND: even populations (sampled), 0-based index 2k+1
   static constexpr int NO = (N + 1) / 2;     // COND: odd populations (analytic), 0-based index 2j
-  static constexpr int L = 4 / cgcd(U, 4);                        // draws per Philox-aligned step
-  static constexpr int BLOCKS = U * L / 4;                        // Philox blocks per step
+  static constexpr int R = (EST == 0) ? 2 : 1;                    // samples per record
+  static constexpr int NPAIR = (EST == 0) ? P : (NNORM + 1) / 2;  // Box-Muller pairs per record
+  static constexpr int WR = (EST == 0) ? 2 * P + 2 * NE : 2 * NPAIR;   // words per record
+  static constexpr int LR = 4 / cgcd(WR, 4);                      // records per Philox-aligned step
+  static constexpr int L = R * LR;                                // samples per step
+  static constexpr int BLOCKS = LR * WR / 4;                      // Philox blocks per step
   static constexpr int NM = N * (N + 1) / 2;                      // packed lower-triangular M
   static constexpr int DUMP = NNORM + N + 1;                      // floats per dumped draw
+  // first word of sample s (s a multiple of R) and of its record
+  static __host__ __device__ constexpr uint64_t word_of(uint64_t s) { return s / R * (uint64_t)WR; }
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -432,21 +438,25 @@ struct Shared {
   float vu[Geo<N, EST, MODEL>::NE > 0 ? Geo<N, EST, MODEL>::NE : 1];   // COND: SOV uniforms v_k
 };
 
+// Box-Muller over the record's NPAIR word pairs: normals 2j, 2j+1 from words 2j (radius), 2j+1 (angle).
 template <int N, int EST, int MODEL>
-__device__ __forceinline__ void draw_shared(const uint32_t* w, uint32_t one, const ProbRegs<N>& pr,
-                                            const StrataRegs* sr, Shared<N, EST, MODEL>& sh, float* nrm_out = nullptr) {
+__device__ __forceinline__ void record_normals(const uint32_t* w, uint32_t one, float* nrm) {
   using G = Geo<N, EST, MODEL>;
-  float nrm[2 * G::NPAIR];
 #pragma unroll
   for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(w[2 * j], w[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
-  if (nrm_out)
-#pragma unroll
-    for (int k = 0; k < G::NNORM; ++k) nrm_out[k] = nrm[k];
+}
+
+// Sample h of a record: its normals start at nrm + h P (COND) and its SOV uniforms at word 2P + h NE.
+template <int N, int EST, int MODEL>
+__device__ __forceinline__ void shared_of_sample(const float* nrm, const uint32_t* w, int h, uint32_t one,
+                                                 const ProbRegs<N>& pr, const StrataRegs* sr, Shared<N, EST, MODEL>& sh) {
+  using G = Geo<N, EST, MODEL>;
+  const float* e = nrm + h * G::P;
   if constexpr (MODEL == 1) {
     static_assert(N == 2, "the C4 strata model has n = 2");
     const float zero[2] = {0.0f, 0.0f};
     float bb[2];
-    strata_b(nrm, zero, *sr, bb);
+    strata_b(e, zero, *sr, bb);
     sh.v[0] = -bb[0];
     sh.v[1] = -bb[1];
   } else {
@@ -455,7 +465,7 @@ __device__ __forceinline__ void draw_shared(const uint32_t* w, uint32_t one, con
     for (int i = 0; i < N; ++i) {
       float acc = 0.0f;
 #pragma unroll
-      for (int j = 0; j <= i; ++j) acc = fmaf(pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
+      for (int j = 0; j <= i; ++j) acc = fmaf(pr.M[i * (i + 1) / 2 + j], e[j], acc);
       sh.v[i] = acc;
     }
   }
@@ -469,9 +479,9 @@ __device__ __forceinline__ void draw_shared(const uint32_t* w, uint32_t one, con
       sh.x[i] = x;
     }
   } else {
-    constexpr int VB = 2 * ((G::P + 1) / 2);
 #pragma unroll
-    for (int k = 0; k < G::NE; ++k) sh.vu[k] = word_to_f12(w[VB + k], one) - 0.99999994039535522f;  // (k+1/2) 2^-23
+    for (int k = 0; k < G::NE; ++k)   // (k+1/2) 2^-23
+      sh.vu[k] = word_to_f12(w[2 * G::P + h * G::NE + k], one) - 0.99999994039535522f;
   }
 }
 
@@ -512,117 +522,56 @@ __device__ __forceinline__ float utility_of_b(const float* b, const Shared<N, ES
   return u;
 }
 
-// Independent draws: b is formed directly from zc (FFMA chains seeded with zc, no separate v).
+// Independent draws: the R utilities of one record, b formed directly from zc (FFMA chains seeded
+// with zc, no separate v).  If DBG, writes per sample the (unscaled) normals, b and u; bsc[i] (the
+// row scales) and BM_K undo the folding for the dump.
 template <int N, int EST, bool DBG, int MODEL = 0>
-__device__ __forceinline__ float draw_utility(const uint32_t* w, uint32_t one, const float* zc, const ProbRegs<N>& pr,
-                                              float* dbg = nullptr, const float* bsc = nullptr,
-                                              const StrataRegs* sr = nullptr) {
+__device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, const float* zc, const ProbRegs<N>& pr,
+                                               const StrataRegs* sr, float* u, float* dbg = nullptr,
+                                               const float* bsc = nullptr) {
   using G = Geo<N, EST, MODEL>;
-  Shared<N, EST, MODEL> sh;
   float nrm[2 * G::NPAIR];
-  float b[N];
-  if constexpr (MODEL == 1) {
-    draw_shared<N, EST, MODEL>(w, one, pr, sr, sh, nrm);
+  record_normals<N, EST, MODEL>(w, one, nrm);
 #pragma unroll
-    for (int i = 0; i < N; ++i) b[i] = zc[i] - sh.v[i];
-  } else {
+  for (int h = 0; h < G::R; ++h) {
+    Shared<N, EST, MODEL> sh;
+    float b[N];
+    const float* e = nrm + h * G::P;
+    if constexpr (MODEL == 1) {
+      shared_of_sample<N, EST, MODEL>(nrm, w, h, one, pr, sr, sh);
 #pragma unroll
-    for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(w[2 * j], w[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      float acc = zc[i];
-#pragma unroll
-      for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
-      b[i] = acc;
-    }
-    if constexpr (EST == 1) {
-      float x = nrm[G::P];
-      sh.x[0] = x;
-#pragma unroll
-      for (int i = 1; i < N; ++i) {
-        x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * nrm[G::P + i]);
-        sh.x[i] = x;
-      }
+      for (int i = 0; i < N; ++i) b[i] = zc[i] - sh.v[i];
     } else {
-      constexpr int VB = 2 * ((G::P + 1) / 2);
-#pragma unroll
-      for (int k = 0; k < G::NE; ++k) sh.vu[k] = word_to_f12(w[VB + k], one) - 0.99999994039535522f;
-    }
-  }
-  const float u = utility_of_b<N, EST, MODEL>(b, sh, pr);
-  if constexpr (DBG) {
-#pragma unroll
-    for (int k = 0; k < G::NNORM; ++k) dbg[k] = nrm[k] * BM_K;
-#pragma unroll
-    for (int i = 0; i < N; ++i) dbg[G::NNORM + i] = b[i] / bsc[i];
-    dbg[G::NNORM + N] = u;
-  }
-  return u;
-}
-
-// COND with the L draws of a Philox step evaluated stage by stage, so the rare deep-tail inverse-CDF
-// branch is taken once per stage for the whole step instead of once per draw (one large basic block
-// per stage for the scheduler).  Same arithmetic, draw by draw, as draw_utility.
-template <int N, int EST, int MODEL, int L>
-__device__ __forceinline__ void draw_utility_batch(const uint32_t* w, uint32_t one, const float* zc,
-                                                   const ProbRegs<N>& pr, const StrataRegs* sr, float* u) {
-  using G = Geo<N, EST, MODEL>;
-  if constexpr (EST == 1 || MODEL == 1 || G::NE == 0) {
-#pragma unroll
-    for (int l = 0; l < L; ++l) u[l] = draw_utility<N, EST, false, MODEL>(&w[l * G::U], one, zc, pr, nullptr, nullptr, sr);
-  } else {
-    constexpr int VB = 2 * ((G::P + 1) / 2);
-    float b[L][N];
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-      const uint32_t* wl = &w[l * G::U];
-      float nrm[2 * G::NPAIR];
-#pragma unroll
-      for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(wl[2 * j], wl[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         float acc = zc[i];
 #pragma unroll
-        for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], nrm[j], acc);
-        b[l][i] = acc;
+        for (int j = 0; j <= i; ++j) acc = fmaf(-pr.M[i * (i + 1) / 2 + j], e[j], acc);
+        b[i] = acc;
+      }
+      if constexpr (EST == 1) {
+        float x = nrm[G::P];
+        sh.x[0] = x;
+#pragma unroll
+        for (int i = 1; i < N; ++i) {
+          x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * nrm[G::P + i]);
+          sh.x[i] = x;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < G::NE; ++k) sh.vu[k] = word_to_f12(w[2 * G::P + h * G::NE + k], one) - 0.99999994039535522f;
       }
     }
-    float x[L][G::NE];
+    u[h] = utility_of_b<N, EST, MODEL>(b, sh, pr);
+    if constexpr (DBG) {
+      float* o = dbg + h * G::DUMP;
 #pragma unroll
-    for (int k = 0; k < G::NE; ++k) {
-      float p[L], pc[L], wq[L], y[L];
-      bool deep = false;
+      for (int k = 0; k < G::P; ++k) o[k] = e[k] * BM_K;
 #pragma unroll
-      for (int l = 0; l < L; ++l) {
-        const float a = k == 0 ? b[l][1] : fmaf(-pr.er[k], x[l][k - 1], b[l][2 * k + 1]);
-        float q, e;
-        normal_tail(a, q, e);
-        u[l] = k == 0 ? q : fmaf(1.0f - u[l], q, u[l]);
-        const float v = word_to_f12(w[l * G::U + VB + k], one) - 0.99999994039535522f;
-        p[l] = v * e;
-        pc[l] = fmaf(v, q, 1.0f - v);
-        y[l] = quantile_main(p[l], pc[l], wq[l]);
-        deep = deep || (wq[l] >= 16.0f);
-      }
-      if (deep) {
+      for (int k = G::P; k < G::NNORM; ++k) o[k] = nrm[k] * BM_K;   // IND null normals (R = 1)
 #pragma unroll
-        for (int l = 0; l < L; ++l)
-          if (wq[l] >= 16.0f) y[l] = quantile_deep(p[l], pc[l], wq[l]);
-      }
-#pragma unroll
-      for (int l = 0; l < L; ++l) x[l][k] = k == 0 ? y[l] : fmaf(pr.esd[k], y[l], pr.emu[k] * x[l][k - 1]);
-    }
-#pragma unroll
-    for (int j = 0; j < G::NO; ++j) {
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        float a = b[l][2 * j];
-        if (2 * j >= 1) a = fmaf(-pr.oa[j], x[l][j - 1], a);
-        if (2 * j + 1 < N) a = fmaf(-pr.ob[j], x[l][j], a);
-        float q, e;
-        normal_tail(a, q, e);
-        u[l] = fmaf(1.0f - u[l], q, u[l]);
-      }
+      for (int i = 0; i < N; ++i) o[G::NNORM + i] = b[i] / bsc[i];
+      o[G::NNORM + N] = u[h];
     }
   }
 }

@@ -61,6 +61,10 @@ __device__ __forceinline__ void accumulate(float u, uint32_t& a1, uint32_t& a2) 
   if constexpr (EST == 0) a2 += __float_as_uint(fmaf(u, u, 1.0f)) - 0x3F800000u;
 }
 
+#ifndef MC_STEP_UNROLL
+#define MC_STEP_UNROLL 1
+#endif
+constexpr int kStepUnroll = MC_STEP_UNROLL;   // steady-loop unroll (pragma arguments are not macro-expanded)
 template <int N, int EST, bool MASKED, int MODEL>
 __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64_t E, uint32_t lo1d, uint32_t hi1d,
                                             const RoundKeys& rk, const float* zc, const ProbRegs<N>& pr,
@@ -68,7 +72,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
   using G = Geo<N, EST, MODEL>;
   constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
   static_assert(SAMPLES_PER_THREAD % G::L == 0, "L must divide the per-thread run");
-  uint64_t q = s_begin * (uint64_t)G::U / 4;   // first Philox block of this thread's run
+  uint64_t q = G::word_of(s_begin) / 4;   // first Philox block of this thread's run
   const uint32_t one = one_bits_reg();
   if constexpr (!MASKED) {
     // steady state: the run's Philox counters q .. q + STEPS*BLOCKS share q_hi unless the low word wraps
@@ -77,22 +81,19 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
     if (q0 <= 0xFFFFFFFFu - NBLK) {
       const uint32_t c0r1 = hi1d ^ (uint32_t)(q >> 32) ^ rk.k0[0];
       uint32_t ql = q0;
-#pragma unroll 1
+#pragma unroll kStepUnroll
       for (int st = 0; st < STEPS; ++st) {
         uint32_t w[G::BLOCKS * 4];
 #pragma unroll
         for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk.k1[0], rk, &w[4 * b]);
         ql += G::BLOCKS;
-#if MC_BATCH_TAIL
-        float uu[G::L];
-        draw_utility_batch<N, EST, MODEL, G::L>(w, one, zc, pr, &sr, uu);
 #pragma unroll
-        for (int l = 0; l < G::L; ++l) accumulate<EST>(uu[l], a1, a2);
-#else
+        for (int r = 0; r < G::LR; ++r) {
+          float u[G::R];
+          record_utility<N, EST, false, MODEL>(&w[r * G::WR], one, zc, pr, &sr, u);
 #pragma unroll
-        for (int l = 0; l < G::L; ++l)
-          accumulate<EST>(draw_utility<N, EST, false, MODEL>(&w[l * G::U], one, zc, pr, nullptr, nullptr, &sr), a1, a2);
-#endif
+          for (int h = 0; h < G::R; ++h) accumulate<EST>(u[h], a1, a2);
+        }
       }
       if constexpr (EST == 1) a2 = a1;
       return;
@@ -107,13 +108,17 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
     for (int b = 0; b < G::BLOCKS; ++b) philox_block_rk(q + b, lo1d, hi1d, rk, &w[4 * b]);
     q += G::BLOCKS;
 #pragma unroll
-    for (int l = 0; l < G::L; ++l) {
-      float u = draw_utility<N, EST, false, MODEL>(&w[l * G::U], one, zc, pr, nullptr, nullptr, &sr);
-      if (MASKED) {
-        const uint64_t s = s0 + l;
-        u = (s >= B && s < E) ? u : 0.0f;
+    for (int r = 0; r < G::LR; ++r) {
+      float u[G::R];
+      record_utility<N, EST, false, MODEL>(&w[r * G::WR], one, zc, pr, &sr, u);
+#pragma unroll
+      for (int h = 0; h < G::R; ++h) {
+        if (MASKED) {
+          const uint64_t s = s0 + r * G::R + h;
+          u[h] = (s >= B && s < E) ? u[h] : 0.0f;
+        }
+        accumulate<EST>(u[h], a1, a2);
       }
-      accumulate<EST>(u, a1, a2);
     }
   }
   if constexpr (EST == 1) a2 = a1;
@@ -174,9 +179,6 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused
 // uniforms) is computed once and reused for a block of CRN_KD designs held in registers.
 // designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 4 / 2,
 // IND 16 / 4
-#ifndef MC_BATCH_TAIL
-#define MC_BATCH_TAIL 0
-#endif
 #ifndef MC_CRN_KD_COND
 #define MC_CRN_KD_COND 4
 #endif
@@ -199,7 +201,7 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
   constexpr int STEPS = SAMPLES_PER_THREAD / G::L;
   const uint32_t one = one_bits_reg();
   const uint32_t lo1d = 0xCD9E8D57u * pid, hi1d = __umulhi(0xCD9E8D57u, pid);
-  uint64_t q = s_begin * (uint64_t)G::U / 4;
+  uint64_t q = G::word_of(s_begin) / 4;
   const uint32_t k1r1 = rk.k1[0] ^ 1u;   // counter word 3 = tag 1
 #pragma unroll 1
   for (int st = 0; st < STEPS; ++st) {
@@ -213,22 +215,28 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
     }
     q += G::BLOCKS;
 #pragma unroll
-    for (int l = 0; l < G::L; ++l) {
-      Shared<N, EST, MODEL> sh;
-      draw_shared<N, EST, MODEL>(&w[l * G::U], one, pr, &sr, sh);
-      bool valid = true;
-      if (MASKED) {
-        const uint64_t s = s0 + l;
-        valid = s >= B && s < E;
-      }
+    for (int r = 0; r < G::LR; ++r) {
+      const uint32_t* wr = &w[r * G::WR];
+      float nrm[2 * G::NPAIR];
+      record_normals<N, EST, MODEL>(wr, one, nrm);
 #pragma unroll
-      for (int k = 0; k < KD; ++k) {
-        float b[N];
+      for (int h = 0; h < G::R; ++h) {
+        Shared<N, EST, MODEL> sh;
+        shared_of_sample<N, EST, MODEL>(nrm, wr, h, one, pr, &sr, sh);
+        bool valid = true;
+        if (MASKED) {
+          const uint64_t s = s0 + r * G::R + h;
+          valid = s >= B && s < E;
+        }
 #pragma unroll
-        for (int i = 0; i < N; ++i) b[i] = zc[k][i] - sh.v[i];
-        float u = utility_of_b<N, EST, MODEL>(b, sh, pr);
-        if (MASKED) u = valid ? u : 0.0f;
-        accumulate<EST>(u, a1[k], a2[k]);
+        for (int k = 0; k < KD; ++k) {
+          float b[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) b[i] = zc[k][i] - sh.v[i];
+          float u = utility_of_b<N, EST, MODEL>(b, sh, pr);
+          if (MASKED) u = valid ? u : 0.0f;
+          accumulate<EST>(u, a1[k], a2[k]);
+        }
       }
     }
   }
@@ -416,9 +424,9 @@ mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64
 }
 
 int words_per_draw(int n, int est, int model) {
-  // Geo<N,EST,MODEL>::U without instantiating every N
+  // Geo<N,EST,MODEL>::WR / R (words per sample) without instantiating every N
   const int p = model == 1 ? 5 : n;
-  return est == 0 ? 2 * ((p + 1) / 2) + n / 2 : 2 * ((p + n + 1) / 2);
+  return est == 0 ? p + n / 2 : 2 * ((p + n + 1) / 2);
 }
 int draw_dump_stride(int n, int est, int model) {
   const int p = model == 1 ? 5 : n;
@@ -487,7 +495,7 @@ mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64
   return MC_OK;
 }
 
-// Per-draw dump through the fused kernel's draw_utility (test hook).
+// Per-draw dump through the fused kernel's record_utility (test hook).
 template <int N, int EST, int MODEL, bool CRN>
 __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restrict__ zc_all,
                             const int32_t* __restrict__ pod, uint64_t seed, const int64_t* __restrict__ design,
@@ -502,13 +510,17 @@ __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restr
   if constexpr (MODEL == 1) load_strata(prob + (int64_t)pod[d] * PROB_STRIDE, sr);
   float zc[N];
   for (int k = 0; k < N; ++k) zc[k] = zc_all[d * N + k];
-  uint32_t w[G::U];
-  const uint64_t base = sample[i] * (uint64_t)G::U;
-  for (int k = 0; k < G::U; ++k)
+  // the whole record of the sample, then its half h
+  uint32_t w[G::WR];
+  const uint64_t base = G::word_of(sample[i] - sample[i] % G::R);
+  const int h = (int)(sample[i] % G::R);
+  for (int k = 0; k < G::WR; ++k)
     w[k] = CRN ? philox_word_tagged(seed, (uint32_t)pod[d], 1u, base + k) : philox_word(seed, (uint32_t)d, base + k);
   float bsc[N];
   for (int k = 0; k < N; ++k) bsc[k] = prob[(int64_t)pod[d] * PROB_STRIDE + OFF_BSC + k];
-  draw_utility<N, EST, true, MODEL>(w, 0x3F800000u, zc, pr, out + i * G::DUMP, bsc, &sr);
+  float u[G::R], dbg[G::R * G::DUMP];
+  record_utility<N, EST, true, MODEL>(w, 0x3F800000u, zc, pr, &sr, u, dbg, bsc);
+  for (int k = 0; k < G::DUMP; ++k) out[i * G::DUMP + k] = dbg[h * G::DUMP + k];
 }
 
 template <int N, int EST, int MODEL = 0>

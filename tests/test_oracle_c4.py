@@ -16,7 +16,7 @@ def _mc(O, r2, sp, alpha, est, N, design=0):
 
 
 def test_words_per_draw_c4(O):
-    assert O.words_per_draw(2, 5, 0) == 7      # 3 Box-Muller pairs + 1 SOV uniform
+    assert O.words_per_draw(2, 5, 0) == 6      # per sample pair: 5 Box-Muller pairs + 2 SOV uniforms
     assert O.words_per_draw(2, 5, 1) == 8      # 7 normals -> 4 pairs
 
 

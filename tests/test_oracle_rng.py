@@ -38,13 +38,51 @@ def test_word_stream_layout(O):
 
 
 def test_words_per_draw(O):
-    # COND: 2*ceil(p/2) Box-Muller words + floor(n/2) SOV uniforms (even populations); IND: 2*ceil((p+n)/2)
-    assert O.words_per_draw(3, 3, 0) == 5
+    # COND: a record of two samples takes p Box-Muller pairs (2p words) + 2 floor(n/2) SOV uniforms,
+    # i.e. p + floor(n/2) words per sample; IND: 2*ceil((p+n)/2) words per sample
+    assert O.words_per_draw(3, 3, 0) == 4
     assert O.words_per_draw(3, 3, 1) == 6
-    assert O.words_per_draw(1, 1, 0) == 2
+    assert O.words_per_draw(1, 1, 0) == 1
     assert O.words_per_draw(2, 2, 0) == 3
     assert O.words_per_draw(10, 10, 0) == 15
     assert O.words_per_draw(10, 10, 1) == 20
+
+
+def _bm(word_r, word_a):
+    # u_r = 1 - k 2^-23, u_a = k 2^-23 from the low 23 bits; R = sqrt(-2 ln u_r)
+    ur = 1.0 - (word_r & 0x7FFFFF) * 2.0 ** -23
+    ua = (word_a & 0x7FFFFF) * 2.0 ** -23
+    R = math.sqrt(-2.0 * math.log(ur))
+    return R * math.cos(2 * math.pi * ua), R * math.sin(2 * math.pi * ua)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+def test_cond_record_layout(O, n):
+    # COND sample pair (2j, 2j+1) = words [jW, (j+1)W), W = 2n + 2(n/2): sample 2j takes the normals
+    # [0, n) of the record's n Box-Muller pairs, sample 2j+1 the normals [n, 2n)
+    seed, d = 0x2005105494, 11
+    r = [1.0, 0.6, 0.35, 0.2][:n]
+    prob = O.point_mass_problem(r, [0.0] * n, 100.0)
+    W = 2 * n + 2 * (n // 2)
+    for j in [0, 1, 7, 123457]:
+        z = []
+        for t in range(n):
+            z.extend(_bm(O.word(seed, d, j * W + 2 * t), O.word(seed, d, j * W + 2 * t + 1)))
+        for h in range(2):
+            eps = O.draw(prob, [0.01] * n, O.EST_COND, seed, d, 2 * j + h)["eps"]
+            assert np.allclose(eps, z[h * n:(h + 1) * n], rtol=1e-13, atol=1e-13)
+
+
+def test_cond_pair_halves_independent(O):
+    # the two samples of a record share Box-Muller pairs when p is odd (one pair splits across them);
+    # the halves must still be independent N(0, I): corr(eps_2j, eps_2j+1) ~ 0, moments of N(0, 1)
+    prob = O.point_mass_problem([1, 0.5, 0.25], [0.0, 0.0, 0.0], 100.0)
+    eps = np.array([O.draw(prob, [0.01] * 3, O.EST_COND, 99, 5, s)["eps"] for s in range(20000)])
+    N = eps.shape[0]
+    assert np.all(np.abs(eps.mean(0)) < 5 / math.sqrt(N)) and np.all(np.abs(eps.var(0) - 1) < 5 * math.sqrt(2 / N))
+    a, b = eps[0::2], eps[1::2]
+    C = np.corrcoef(np.hstack([a, b]).T)
+    assert np.all(np.abs(C[np.triu_indices(6, 1)]) < 5 / math.sqrt(N / 2))
 
 
 def test_word_bits_uniform(O):

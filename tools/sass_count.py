@@ -18,10 +18,11 @@ import sys
 
 LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2005_10494_b200", "libmc_design.so")
 def draws_per_iter(n: int, est: int) -> int:
-    """L = 4 / gcd(U, 4) draws per Philox-aligned step (mc_device.cuh Geo)."""
+    """L = R * 4 / gcd(WR, 4) samples per Philox-aligned step (mc_device.cuh Geo): COND records are
+    sample pairs of WR = 2n + 2(n/2) words, IND records single samples of 2n words."""
     import math
-    U = 2 * ((n + 1) // 2) + n // 2 if est == 0 else 2 * n
-    return 4 // math.gcd(U, 4)
+    R, WR = (2, 2 * n + 2 * (n // 2)) if est == 0 else (1, 2 * n)
+    return R * (4 // math.gcd(WR, 4))
 
 
 def sass(n: int, est: int, lib: str = None, model: int = 0):
