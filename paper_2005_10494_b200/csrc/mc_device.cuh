@@ -277,12 +277,13 @@ __device__ __forceinline__ float normal_quantile(float p, float pc) {
 __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
   constexpr double S2 = 1.4142135623730950488;
   // p pc may flush to 0 (e ~ 0): lg2 -> -inf, w -> +inf, handled by the deep-tail clamp
-  const float w = -0.69314718056f * (lg2_approx(p * pc) + 2.0f);
 #if MC_QUANTILE_BRANCHFREE
   // w in [0, 16) (p in [1.1e-7, 1 - 1.1e-7]): ONE degree-12 polynomial in sqrt(w + 2)
   // (tools/fit_erfinv_single.py, relative error 5.3e-7 in fp32) -- no per-coefficient selects on the
   // ALU pipe; the deep tail w >= 16 (e_i < ~1e-7) takes a rare divergent branch.
-  const float x = sqrt_approx(w + 2.0f) - 2.82842712474619f;
+  // w + 2 = -ln2 lg2(p pc) + (2 - 2 ln2) in one FFMA.
+  const float w2 = fmaf(lg2_approx(p * pc), -0.69314718056f, 0.61370563888f);
+  const float x = sqrt_approx(w2) - 2.82842712474619f;
   float g = -0.0001458914359425521f;
   g = fmaf(g, x, 0.00014054195626482066f);
   g = fmaf(g, x, 0.0012376677239334937f);
@@ -296,8 +297,8 @@ __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
   g = fmaf(g, x, -0.018363709814932894f);
   g = fmaf(g, x, 1.59782737417905f);
   g = fmaf(g, x, 3.2334928032079135f);
-  if (w >= 16.0f) {
-    const float ww = sqrt_approx(fminf(w, 88.0f)) - 6.0f;
+  if (w2 >= 18.0f) {
+    const float ww = sqrt_approx(fminf(w2 - 2.0f, 88.0f)) - 6.0f;
     g = (float)(7.926354328446905e-07 * S2);
     g = fmaf(g, ww, (float)(-6.932396900083404e-06 * S2));
     g = fmaf(g, ww, (float)(2.5214179913746193e-05 * S2));
@@ -308,6 +309,7 @@ __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
   }
   return g * (p - pc);
 #else
+  const float w = -0.69314718056f * (lg2_approx(p * pc) + 2.0f);
   float g;
   if (w < 5.0f) {
     const float ww = w - 2.5f;
@@ -494,7 +496,7 @@ __device__ __forceinline__ float utility_of_b(const float* b, const Shared<N, ES
     // success iff some X_i > b_i
     bool rej = sh.x[0] > b[0];
 #pragma unroll
-    for (int i = 1; i < N; ++i) rej = rej || (sh.x[i] > b[i]);
+    for (int i = 1; i < N; ++i) rej = rej | (sh.x[i] > b[i]);   // FSETP.OR chain, no short circuit
     u = rej ? 1.0f : 0.0f;
   } else {
     // COND: u = 1 - prod e accumulated as u <- u + (1 - u) q (q = 1 - e: no cancellation).

@@ -60,6 +60,25 @@ __device__ __forceinline__ void accumulate(float u, uint32_t& a1, uint32_t& a2) 
   a1 += __float_as_uint(u + 1.0f) - 0x3F800000u;
   if constexpr (EST == 0) a2 += __float_as_uint(fmaf(u, u, 1.0f)) - 0x3F800000u;
 }
+// Steady-state form: the raw bit patterns are summed modulo 2^32 and the constant 0x3F800000 per draw
+// is removed once per run (finish_biased); exact because the true sum stays below 2^31.
+// (COND only: the IND indicator already folds into one select per draw.)
+template <int EST>
+__device__ __forceinline__ void accumulate_biased(float u, uint32_t& a1, uint32_t& a2) {
+  if constexpr (EST == 0) {
+    a1 += __float_as_uint(u + 1.0f);
+    a2 += __float_as_uint(fmaf(u, u, 1.0f));
+  } else {
+    accumulate<EST>(u, a1, a2);
+  }
+}
+template <int EST>
+__device__ __forceinline__ void finish_biased(uint32_t draws, uint32_t& a1, uint32_t& a2) {
+  if constexpr (EST == 0) {
+    a1 -= draws * 0x3F800000u;
+    a2 -= draws * 0x3F800000u;
+  }
+}
 
 #ifndef MC_STEP_UNROLL
 #define MC_STEP_UNROLL 1
@@ -92,9 +111,10 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
           float u[G::R];
           record_utility<N, EST, false, MODEL>(&w[r * G::WR], one, zc, pr, &sr, u);
 #pragma unroll
-          for (int h = 0; h < G::R; ++h) accumulate<EST>(u[h], a1, a2);
+          for (int h = 0; h < G::R; ++h) accumulate_biased<EST>(u[h], a1, a2);
         }
       }
+      finish_biased<EST>(SAMPLES_PER_THREAD, a1, a2);
       if constexpr (EST == 1) a2 = a1;
       return;
     }

@@ -5,6 +5,8 @@ target of its backward branch along the COMMON path:
   * `BRA.DIV` (divergence fallback of a warp vote) is not taken;
   * `@!P BRA` right after `VOTE.ANY P` (the warp-uniform rare inverse-CDF tail) is taken, i.e. the
     tail polynomials are skipped;
+  * a branch on a predicate last written by `FSETP.GE[U] P, PT, R, {5, 16, 18}` (the inverse-CDF tail
+    tests w >= 5, w >= 16, w + 2 >= 18: rare) goes the common way: `@!P BRA` taken, `@P BRA` not;
   * unconditional forward `BRA` is followed; other conditional forward branches fall through.
 Issue slots per draw = path length / draws per iteration.  Used by bench.py for the ALU roofline.
 
@@ -55,17 +57,28 @@ def walk(ins, start, end):
     i = idx[start]
     path = []
     prev = ""
+    rare = {}          # predicate -> True if last written by a rare-tail FSETP
     for _ in range(20000):
         a, t = ins[i]
         path.append((a, t))
         if a == end:
             break
+        m = re.match(r"FSETP\.(\w+)\.AND (P\d), PT, [^,]+, ([0-9.e+-]+), PT", t)
+        if m:
+            rare[m.group(2)] = m.group(1) in ("GE", "GEU") and float(m.group(3)) in (5.0, 16.0, 18.0)
+        else:
+            m = re.match(r"\w+(?:\.\w+)* (P\d),", t)
+            if m and not t.startswith("@"):
+                rare[m.group(1)] = False
         tgt = _target(t)
+        pm = re.match(r"@(!?)(P\d) BRA", t)
         if tgt is not None and "BRA" in t:
             if "BRA.DIV" in t:
                 i += 1
             elif t.startswith("@!P") and prev.startswith("VOTE.ANY P"):
                 i = idx[tgt]
+            elif pm and rare.get(pm.group(2)):
+                i = idx[tgt] if pm.group(1) == "!" else i + 1
             elif t.startswith("@P") and ("FSETP.GEU" in prev and (", 5," in prev or ", 16," in prev)):
                 i += 1          # w >= 5 / w >= 16: the inverse-CDF tails, not taken on the common path
             elif not t.startswith("@") and tgt > a:
