@@ -137,7 +137,9 @@ mc_status mc_design_upload(mc_ctx* ctx, const double* alpha_host, void* cuda_str
 mc_status mc_set_sampling(mc_ctx* ctx, int32_t mode);
 
 /* Launch shape of the fused kernel (results do not depend on it): threads per block (multiple of
- * 32 in [32, 256]; 0 = default 256) and grid blocks (>= 0; 0 = #SMs x max resident blocks). */
+ * 32 in [32, 256]; 0 = default 256) and grid blocks (>= 0; 0 = one 4096-sample warp tile per warp,
+ * balanced by the hardware block scheduler; > 0 = a persistent grid of that many blocks striding over
+ * the tiles); the same for the common-random-numbers kernel. */
 mc_status mc_set_launch(mc_ctx* ctx, int32_t block_threads, int32_t grid_blocks);
 
 void mc_destroy(mc_ctx* ctx);
