@@ -228,6 +228,19 @@ mc_status mc_surface_eval(const mc_surface* s, const double* x_host, int64_t q, 
 mc_status mc_surface_max(const mc_surface* s, double* x_out_host, double* f_out_host);
 void mc_surface_destroy(mc_surface* s);
 
+/* ---- a9 for dense regular grids (configuration C4, R23) ------- */
+
+/* Separable Gaussian (Nadaraya-Watson) kernel smoother of a regular design grid:
+ * smoothed_dev = S_r values_dev S_a^T, values_dev[nr*na] row-major (row i: coordinate xr_host[i], column j:
+ * xa_host[j]; both strictly increasing, 2 <= nr, na <= 4096), S_x the row-normalised weights
+ * exp(-(x_i - x_k)^2 / (2 h_x^2)).  hr, ha > 0: those bandwidths; otherwise both are chosen jointly by GCV
+ * over h = 2^(j/2) x (mean grid step), j = -2..8 (first minimiser, r bandwidth outer).  h_used_host[2]
+ * (may be NULL) receives (hr, ha).  fp64, device pointers in/out (in-place allowed), caller's stream;
+ * synchronises (the GCV choice is made on the host).  MC_ERR_INVALID on bad sizes/coordinates. */
+mc_status mc_grid_smooth(const double* values_dev, int32_t nr, int32_t na, const double* xr_host,
+                         const double* xa_host, double hr, double ha, double* smoothed_dev, double* h_used_host,
+                         void* cuda_stream);
+
 /* ---- a10: argmax --------------------------------------------------------------- */
 
 /* Per problem: the design with the largest value (lowest index on ties; NaN never wins) ->

@@ -531,3 +531,52 @@ def finalize_crossed(sums, n1: int, n2: int):
     mean = S[:, 0] / (n1 * n2)
     var = (S[:, 1] / (n2 * n2) - n1 * mean * mean) / max(n1 - 1, 1)
     return mean, var
+
+
+# --------------------------------------------------------------------------------------
+# C4 dense-grid smoother (SURVEY §8(a) a9 "Dense regular grids (C4)"; reading R23 in DESIGN.md):
+# the separable Gaussian (Nadaraya-Watson) kernel smoother P~ = S_r P^ S_a^T over the (r2, alpha_1) grid,
+# S_x = row-normalised W_x, W_x[i, k] = exp(-(x_i - x_k)^2 / (2 h_x^2)).  Bandwidths h = k * (grid step)
+# with k in GRID_H_STEPS, chosen jointly by GCV (first minimiser, r-bandwidth outer), tr S = tr S_r tr S_a.
+
+GRID_H_STEPS = 2.0 ** (np.arange(-2, 9) / 2.0)   # 0.5 ... 16 grid steps, ratio sqrt(2)
+
+
+def kernel_matrix_nw(x, h: float) -> np.ndarray:
+    """Row-normalised Gaussian kernel weights on the 1-D coordinates x with bandwidth h."""
+    x = np.asarray(x, dtype=np.float64)
+    W = np.exp(-0.5 * ((x[:, None] - x[None, :]) / h) ** 2)
+    return W / W.sum(axis=1, keepdims=True)
+
+
+def grid_kernel_smooth(P, xr, xa, hr: float, ha: float):
+    """P~ = S_r P S_a^T for P[nr, na] (rows: r coordinate xr, columns: alpha coordinate xa);
+    returns (P~, tr S)."""
+    Sr, Sa = kernel_matrix_nw(xr, hr), kernel_matrix_nw(xa, ha)
+    P = np.asarray(P, dtype=np.float64)
+    return Sr @ P @ Sa.T, float(np.trace(Sr) * np.trace(Sa))
+
+
+def grid_gcv(P, xr, xa, hr: float, ha: float) -> float:
+    """GCV(h) = (1/n) ||P - P~||^2 / (1 - tr S / n)^2 (Craven & Wahba, as for the TPS)."""
+    Ps, tr = grid_kernel_smooth(P, xr, xa, hr, ha)
+    n = Ps.size
+    res = np.asarray(P, dtype=np.float64) - Ps
+    return float((res * res).sum() / n / (1.0 - tr / n) ** 2)
+
+
+def grid_smooth(P, xr, xa, hr: float = -1.0, ha: float = -1.0):
+    """Smoothed grid and the bandwidths used; hr, ha <= 0: GCV over GRID_H_STEPS x the grid steps."""
+    xr, xa = np.asarray(xr, dtype=np.float64), np.asarray(xa, dtype=np.float64)
+    if hr <= 0 or ha <= 0:
+        sr = (xr[-1] - xr[0]) / (len(xr) - 1)
+        sa = (xa[-1] - xa[0]) / (len(xa) - 1)
+        best = None
+        for kr in GRID_H_STEPS:
+            for ka in GRID_H_STEPS:
+                g = grid_gcv(P, xr, xa, kr * sr, ka * sa)
+                if best is None or g < best[0]:
+                    best = (g, kr * sr, ka * sa)
+        hr, ha = best[1], best[2]
+    Ps, _ = grid_kernel_smooth(P, xr, xa, hr, ha)
+    return Ps, (hr, ha)

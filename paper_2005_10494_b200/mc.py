@@ -82,6 +82,7 @@ def lib() -> ctypes.CDLL:
         L.mc_surface_max.argtypes = [vp, P(d), P(d)]; L.mc_surface_max.restype = i32
         L.mc_surface_destroy.argtypes = [vp]; L.mc_surface_destroy.restype = None
         L.mc_argmax.argtypes = [vp, vp, vp, vp, P(i64), P(d), vp]; L.mc_argmax.restype = i32
+        L.mc_grid_smooth.argtypes = [vp, i32, i32, P(d), P(d), d, d, vp, P(d), vp]; L.mc_grid_smooth.restype = i32
         L.mc_num_designs.argtypes = [vp]; L.mc_num_designs.restype = i64
         L.mc_num_problems.argtypes = [vp]; L.mc_num_problems.restype = i32
         L.mc_words_per_draw.argtypes = [vp]; L.mc_words_per_draw.restype = i32
@@ -95,7 +96,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer", "mc_candidates",
             "mc_design_init", "mc_design_upload", "mc_set_sampling", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_evaluate_crossed", "mc_finalize_crossed", "mc_finalize", "mc_smooth_plan",
-            "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
+            "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_grid_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
 
 
@@ -404,6 +405,25 @@ class Surface:
                 lib().mc_surface_destroy(self._h)
         except Exception:
             pass
+
+
+def grid_smooth(values, xr, xa, hr: float = -1.0, ha: float = -1.0, out=None, stream=None):
+    """Row a9 for dense regular grids (C4): separable Gaussian kernel smoother of values[nr, na] (a CUDA
+    fp64 tensor, row i at xr[i], column j at xa[j]); hr, ha <= 0: GCV.  Returns (smoothed, (hr, ha))."""
+    torch = _torch()
+    if not (values.is_cuda and values.dtype == torch.float64 and values.dim() == 2):
+        raise RuntimeError("grid_smooth: values must be a 2-D CUDA float64 tensor (no CPU fallback)")
+    values = values.contiguous()
+    nr, na = values.shape
+    xr = np.ascontiguousarray(xr, dtype=np.float64)
+    xa = np.ascontiguousarray(xa, dtype=np.float64)
+    if xr.shape != (nr,) or xa.shape != (na,):
+        raise ValueError("grid_smooth: coordinate lengths must match the grid")
+    out = torch.empty_like(values) if out is None else out
+    h = (ctypes.c_double * 2)()
+    _check(lib().mc_grid_smooth(values.data_ptr(), nr, na, _dp(xr), _dp(xa), float(hr), float(ha), out.data_ptr(),
+                                h, _stream(stream)))
+    return out, (h[0], h[1])
 
 
 # ------------------------------------------------------------------------------------------

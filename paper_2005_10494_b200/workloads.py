@@ -67,7 +67,7 @@ def c5_problem(n: int):
 
 
 # draws per design (BASELINE.json configs)
-DRAWS = {"C1": 10_000, "C2": 1_000_000, "C3": 1_000_000_000, "C5": 1_000_000}
+DRAWS = {"C1": 10_000, "C2": 1_000_000, "C3": 1_000_000_000, "C4": 1_000_000, "C5": 1_000_000}
 
 
 # C4: synthetic 5-D strata prior (not in the paper), n = 2, dense 256 x 256 design grid

@@ -146,3 +146,43 @@ def test_segmented_argmax_matches_oracle(O, mc, torch):
         seg = np.where(np.isnan(v[off[k]:off[k + 1]]), -np.inf, v[off[k]:off[k + 1]])
         assert idx[k].item() == off[k] + O.argmax(seg)
     assert bi == 2 and bv == 10.0
+
+
+def _gcv_pick_ok(O, P, xr, xa, got_h, ref_h):
+    # identical bandwidths, or a GCV near-tie decided by summation order (scores within 1e-9 relative)
+    if np.allclose(got_h, ref_h, rtol=1e-12):
+        return True
+    g1, g2 = O.grid_gcv(P, xr, xa, *got_h), O.grid_gcv(P, xr, xa, *ref_h)
+    return abs(g1 - g2) <= 1e-9 * abs(g2)
+
+
+@pytest.mark.parametrize("shape", [(7, 5), (64, 48), (256, 256)])
+def test_grid_smooth_matches_oracle(O, mc, torch, shape):
+    """C4 dense-grid smoother (a9, R23): GCV bandwidths and smoothed values against the oracle."""
+    nr, na = shape
+    rng = np.random.default_rng(nr * 1000 + na)
+    xr = (np.arange(nr) + 0.5) / nr
+    xa = (np.arange(na) + 0.5) * 0.025 / na
+    X, Y = np.meshgrid(xr, xa / 0.025, indexing="ij")
+    P = 0.9 - 0.3 * (X - 0.3) ** 2 - 0.2 * (Y - 0.2) ** 2 + 2e-3 * rng.normal(size=(nr, na))
+    ref, ref_h = O.grid_smooth(P, xr, xa)
+    got, got_h = mc.grid_smooth(torch.tensor(P, device="cuda"), xr, xa)
+    assert _gcv_pick_ok(O, P, xr, xa, got_h, ref_h), (got_h, ref_h)
+    ref_at, _ = O.grid_kernel_smooth(P, xr, xa, *got_h)
+    assert np.allclose(got.cpu().numpy(), ref_at, rtol=0, atol=1e-12)
+    # fixed bandwidths, in place
+    t = torch.tensor(P, device="cuda")
+    out, h = mc.grid_smooth(t, xr, xa, 0.07, 0.004, out=t)
+    assert h == (0.07, 0.004)
+    ref2, _ = O.grid_kernel_smooth(P, xr, xa, 0.07, 0.004)
+    assert np.allclose(t.cpu().numpy(), ref2, rtol=0, atol=1e-12)
+
+
+def test_grid_smooth_rejects_bad_input(mc, torch):
+    v = torch.zeros((4, 3), dtype=torch.float64, device="cuda")
+    with pytest.raises(mc.McError):
+        mc.grid_smooth(v, [0.1, 0.2, 0.2, 0.3], [0, 1, 2])          # not strictly increasing
+    with pytest.raises(mc.McError):
+        mc.grid_smooth(torch.zeros((1, 3), dtype=torch.float64, device="cuda"), [0.1], [0, 1, 2])
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        mc.grid_smooth(torch.zeros((4, 3), dtype=torch.float64), [0.1, 0.2, 0.3, 0.4], [0, 1, 2])

@@ -97,3 +97,30 @@ def test_r_sweep_surface_stage_matches_oracle(O, mc, torch):
         xs, fs, _ = O.refine(res.r, res.power_opt, res.lambda_r)
     assert np.allclose(res.r_star, xs, atol=1e-5)
     assert res.power_r_star == pytest.approx(fs, abs=1e-9)
+
+
+def test_c4_grid_optimum_pipeline(O, mc, torch):
+    """C4 end to end at a reduced grid (12 cutoffs x 16 alpha_1, 20k draws): the designs are the oracle's
+    alpha grid, P^ matches the oracle per design, the smoother and the argmax match the oracle applied to
+    the GPU's P^ (the MC noise is shared: both sides see the same Philox draws)."""
+    from paper_2005_10494_b200 import sweep
+    r2s = [(i + 0.5) / 12 for i in range(12)]
+    m, N = 16, 20_000
+    sp = np.array(W.C4_STRATA)
+    g = sweep.c4_grid_optimum(r2s, 211.0, W.C4_STRATA, m, N, W.SEED)
+    assert g.mean.shape == (12, m) and g.smoothed.shape == (12, m)
+    # designs: alpha_1 = (j + 1/2) alpha0 / m with alpha_2 solved (oracle bisection)
+    for i in (0, 5, 11):
+        for j in (0, 7, 15):
+            a1 = (j + 0.5) * 0.025 / m
+            a2 = O.solve_alpha_n([1.0, r2s[i]], 0.025, [a1], 1e-13)
+            d = i * m + j
+            ref_s = O.design_sums_strata(r2s[i], 211.0, sp, [a1, a2], 0, W.SEED, d, 0, N)
+            ref = O.finalize(ref_s, N)[0][0]
+            assert abs(g.mean[i, j] - ref) <= 1e-5 * ref, (i, j, g.mean[i, j], ref)
+    xa = (np.arange(m) + 0.5) * 0.025 / m
+    ref_sm, ref_h = O.grid_smooth(g.mean, np.array(r2s), xa)
+    assert np.allclose(g.bandwidths, ref_h, rtol=1e-12)
+    assert np.allclose(g.smoothed, ref_sm, rtol=0, atol=1e-12)
+    assert g.index == O.argmax(ref_sm.ravel())
+    assert g.r2 == r2s[g.index // m] and g.power_smoothed == pytest.approx(ref_sm.ravel()[g.index], abs=1e-12)

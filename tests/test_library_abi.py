@@ -147,3 +147,19 @@ def test_checkpoint_roundtrip(mc, tmp_path):
     mc.checkpoint_save(str(tmp_path / "ck"), sums, 123456789, 0x2005105494, {"designs": 10})
     s2, done, seed, meta = mc.checkpoint_load(str(tmp_path / "ck"))
     assert np.array_equal(s2, sums) and done == 123456789 and seed == 0x2005105494 and meta["designs"] == 10
+
+
+def test_grid_smooth_validation_before_device(mc):
+    # all argument checks run on the host before any CUDA call (so this runs without a GPU)
+    L = mc.lib()
+    d = ctypes.c_double
+    xr = (d * 4)(0.1, 0.2, 0.3, 0.4)
+    bad = (d * 4)(0.1, 0.3, 0.3, 0.4)
+    xa = (d * 3)(0.0, 1.0, 2.0)
+    fake = ctypes.c_void_p(16)
+    assert L.mc_grid_smooth(None, 4, 3, xr, xa, -1.0, -1.0, fake, None, None) == 1
+    assert L.mc_grid_smooth(fake, 1, 3, xr, xa, -1.0, -1.0, fake, None, None) == 1
+    assert L.mc_grid_smooth(fake, 4, 5000, xr, xa, -1.0, -1.0, fake, None, None) == 1
+    assert L.mc_grid_smooth(fake, 4, 3, bad, xa, -1.0, -1.0, fake, None, None) == 1
+    assert b"strictly increasing" in L.mc_last_error()
+    assert L.mc_grid_smooth(fake, 4, 3, xr, xa, float("inf"), 1.0, fake, None, None) == 1
