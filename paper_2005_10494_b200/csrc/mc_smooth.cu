@@ -323,7 +323,11 @@ static mc_status build_one(mc_ctx* c, PlanLane& ln, TpsPlan& pl, const std::vect
   return MC_OK;
 }
 
-constexpr int PLAN_LANES = 8;   // concurrent plan builders (streams + cuSOLVER handles)
+#ifndef MC_PLAN_LANES
+#define MC_PLAN_LANES 4
+#endif
+constexpr int PLAN_LANES = MC_PLAN_LANES;   // concurrent plan builders (streams + cuSOLVER handles); cuSOLVER Dsyevd
+// barely overlaps across streams: 4 lanes measured best (24 ms/problem at N = 2000; 8 lanes 30-41 ms, 1 lane 28 ms)
 
 mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
   cudaFree(c->d_plan_arena);
