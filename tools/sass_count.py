@@ -6,7 +6,7 @@ target of its backward branch along the COMMON path:
   * `@!P BRA` right after `VOTE.ANY P` (the warp-uniform rare inverse-CDF tail) is taken, i.e. the
     tail polynomials are skipped;
   * a branch on a predicate last written by `FSETP.GE[U] P, PT, R, {5, 16, 18}` (the inverse-CDF tail
-    tests w >= 5, w >= 16, w + 2 >= 18: rare) goes the common way: `@!P BRA` taken, `@P BRA` not;
+    tests w >= 5, w >= 16, w + 2 >= 18, w + 3 >= 27: rare) goes the common way: `@!P BRA` taken, `@P BRA` not;
   * unconditional forward `BRA` is followed; other conditional forward branches fall through.
 Issue slots per draw = path length / draws per iteration.  Used by bench.py for the ALU roofline.
 
@@ -65,7 +65,7 @@ def walk(ins, start, end):
             break
         m = re.match(r"FSETP\.(\w+)\.AND (P\d), PT, [^,]+, ([0-9.e+-]+), PT", t)
         if m:
-            rare[m.group(2)] = m.group(1) in ("GE", "GEU") and float(m.group(3)) in (5.0, 16.0, 18.0)
+            rare[m.group(2)] = m.group(1) in ("GE", "GEU") and float(m.group(3)) in (5.0, 16.0, 18.0, 27.0)
         else:
             m = re.match(r"\w+(?:\.\w+)* (P\d),", t)
             if m and not t.startswith("@"):
