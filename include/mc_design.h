@@ -36,7 +36,8 @@ typedef enum {
 
 typedef enum {
     MC_EST_COND = 0,  /* per-draw utility u = 1 - Phi_Sigma0(b) by one-sample separation of
-                         variables: n normal CDFs + (n-1) inverse CDFs (reading R6) */
+                         variables in the order (even populations, then odd): n normal CDFs +
+                         floor(n/2) inverse CDFs (readings R6, R21) */
     MC_EST_IND = 1    /* the paper's Formula 6/7 indicator with one independent null draw per sample
                          (reading R1) */
 } mc_estimator;
