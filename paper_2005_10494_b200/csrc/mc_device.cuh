@@ -487,6 +487,31 @@ __device__ __forceinline__ void shared_of_sample(const float* nrm, const uint32_
   }
 }
 
+// IND indicator 1[exists i: x_i > b_i] as ONE predicate chain (FSETP, then FSETP.OR per further
+// population) and one select: ptxas otherwise materialises a select per population.
+template <int N>
+__device__ __forceinline__ float ind_indicator(const float* x, const float* b) {
+  float u;
+  if constexpr (N == 1) {
+    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; selp.f32 %0, 0f3F800000, 0f00000000, p; }"
+        : "=f"(u) : "f"(x[0]), "f"(b[0]));
+  } else if constexpr (N == 2) {
+    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p;"
+        " selp.f32 %0, 0f3F800000, 0f00000000, p; }"
+        : "=f"(u) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]));
+  } else if constexpr (N == 3) {
+    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p; setp.gt.or.f32 p, %5, %6, p;"
+        " selp.f32 %0, 0f3F800000, 0f00000000, p; }"
+        : "=f"(u) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]), "f"(x[2]), "f"(b[2]));
+  } else {
+    bool rej = x[0] > b[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) rej = rej | (x[i] > b[i]);
+    u = rej ? 1.0f : 0.0f;
+  }
+  return u;
+}
+
 // The design-dependent part: the utility u in [0, 1] from the thresholds b (= zc - v).
 template <int N, int EST, int MODEL>
 __device__ __forceinline__ float utility_of_b(const float* b, const Shared<N, EST, MODEL>& sh, const ProbRegs<N>& pr) {
@@ -494,10 +519,7 @@ __device__ __forceinline__ float utility_of_b(const float* b, const Shared<N, ES
   float u = 0.0f;
   if constexpr (EST == 1) {
     // success iff some X_i > b_i
-    bool rej = sh.x[0] > b[0];
-#pragma unroll
-    for (int i = 1; i < N; ++i) rej = rej | (sh.x[i] > b[i]);   // FSETP.OR chain, no short circuit
-    u = rej ? 1.0f : 0.0f;
+    u = ind_indicator<N>(sh.x, b);
   } else {
     // COND: u = 1 - prod e accumulated as u <- u + (1 - u) q (q = 1 - e: no cancellation).
     float x[G::NE > 0 ? G::NE : 1];

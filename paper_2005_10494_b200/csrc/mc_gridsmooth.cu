@@ -15,7 +15,6 @@
 
 #include <cmath>
 #include <cstdint>
-#include <mutex>
 #include <vector>
 
 #include "mc_internal.h"
@@ -72,14 +71,14 @@ __global__ void __launch_bounds__(GS_THREADS) k_grid_rss(const double* __restric
 }
 
 namespace {
-std::mutex g_blas_mu;
-cublasHandle_t g_blas[64] = {};
+// One cuBLAS handle per (host thread, device): cublasSetStream on a shared handle would race between
+// threads.  Handles live for the thread (not destroyed at exit: the CUDA context may already be gone).
+thread_local cublasHandle_t t_blas[64] = {};
 
 cublasHandle_t blas_handle(int dev) {
-  std::lock_guard<std::mutex> lk(g_blas_mu);
   if (dev < 0 || dev >= 64) return nullptr;
-  if (!g_blas[dev] && cublasCreate(&g_blas[dev]) != CUBLAS_STATUS_SUCCESS) g_blas[dev] = nullptr;
-  return g_blas[dev];
+  if (!t_blas[dev] && cublasCreate(&t_blas[dev]) != CUBLAS_STATUS_SUCCESS) t_blas[dev] = nullptr;
+  return t_blas[dev];
 }
 
 struct DevBuf {

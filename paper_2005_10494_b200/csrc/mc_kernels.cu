@@ -63,20 +63,23 @@ __device__ __forceinline__ void accumulate(float u, uint32_t& a1, uint32_t& a2) 
 // Steady-state form: the raw bit patterns are summed modulo 2^32 and the constant 0x3F800000 per draw
 // is removed once per run (finish_biased); exact because the true sum stays below 2^31.
 // (COND only: the IND indicator already folds into one select per draw.)
+// IND: u in {0, 1} is counted in an fp32 register (exact up to 2^24 >> 128 draws) and converted once.
 template <int EST>
-__device__ __forceinline__ void accumulate_biased(float u, uint32_t& a1, uint32_t& a2) {
+__device__ __forceinline__ void accumulate_biased(float u, uint32_t& a1, uint32_t& a2, float& cnt) {
   if constexpr (EST == 0) {
     a1 += __float_as_uint(u + 1.0f);
     a2 += __float_as_uint(fmaf(u, u, 1.0f));
   } else {
-    accumulate<EST>(u, a1, a2);
+    cnt += u;
   }
 }
 template <int EST>
-__device__ __forceinline__ void finish_biased(uint32_t draws, uint32_t& a1, uint32_t& a2) {
+__device__ __forceinline__ void finish_biased(uint32_t draws, uint32_t& a1, uint32_t& a2, float cnt) {
   if constexpr (EST == 0) {
     a1 -= draws * 0x3F800000u;
     a2 -= draws * 0x3F800000u;
+  } else {
+    a1 += (uint32_t)cnt << 23;
   }
 }
 
@@ -100,6 +103,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
     if (q0 <= 0xFFFFFFFFu - NBLK) {
       const uint32_t c0r1 = hi1d ^ (uint32_t)(q >> 32) ^ rk.k0[0];
       uint32_t ql = q0;
+      float cnt = 0.0f;
 #pragma unroll kStepUnroll
       for (int st = 0; st < STEPS; ++st) {
         uint32_t w[G::BLOCKS * 4];
@@ -111,10 +115,10 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
           float u[G::R];
           record_utility<N, EST, false, MODEL>(&w[r * G::WR], one, zc, pr, &sr, u);
 #pragma unroll
-          for (int h = 0; h < G::R; ++h) accumulate_biased<EST>(u[h], a1, a2);
+          for (int h = 0; h < G::R; ++h) accumulate_biased<EST>(u[h], a1, a2, cnt);
         }
       }
-      finish_biased<EST>(SAMPLES_PER_THREAD, a1, a2);
+      finish_biased<EST>(SAMPLES_PER_THREAD, a1, a2, cnt);
       if constexpr (EST == 1) a2 = a1;
       return;
     }
