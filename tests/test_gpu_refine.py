@@ -124,3 +124,54 @@ def test_c4_grid_optimum_pipeline(O, mc, torch):
     assert np.allclose(g.smoothed, ref_sm, rtol=0, atol=1e-12)
     assert g.index == O.argmax(ref_sm.ravel())
     assert g.r2 == r2s[g.index // m] and g.power_smoothed == pytest.approx(ref_sm.ravel()[g.index], abs=1e-12)
+
+
+_GRID_CACHE = {}
+
+
+def _grid_designs(O, r, m):
+    """Every feasible point of the half-offset m^(n-1) grid with alpha_n solved by the oracle (cached)."""
+    key = (tuple(r), m)
+    if key not in _GRID_CACHE:
+        _GRID_CACHE[key] = _grid_designs_uncached(O, list(r), m)
+    return _GRID_CACHE[key]
+
+
+def _grid_designs_uncached(O, r, m):
+    n = len(r)
+    rows = []
+    for g in range(m ** (n - 1)):
+        part, t = [], g
+        for _ in range(n - 1):
+            part.append((t % m + 0.5) * 0.025 / m)
+            t //= m
+        part = part[::-1]                       # first coordinate slowest
+        an = O.solve_alpha_n(r, 0.025, part, 1e-13)
+        if an is not None:
+            rows.append(part + [an])
+    return np.array(rows)
+
+
+@pytest.mark.parametrize("r,m", [((1.0, 0.4), 40), ((1.0, 0.75, 0.5, 0.25), 6)])
+@pytest.mark.parametrize("lam", [1e-5, -1.0])
+def test_tps_d1_d3_smooth_and_refine_match_oracle(O, mc, torch, r, m, lam):
+    """The TPS of §2.9 for d = 1 (phi = rho^3, n = 2) and d = 3 (phi = -rho, n = 4, SURVEY f4's TPS):
+    smoothed values, GCV lambda and the f1 continuous optimum against the oracle."""
+    n = len(r)
+    alpha = _grid_designs(O, list(r), m)
+    x = alpha[:, : n - 1] / 0.025
+    y = 0.9 + 0.03 * np.exp(-((x - 0.35) ** 2).sum(1) * 4) + 2e-4 * np.random.default_rng(n).normal(size=len(x))
+    p = mc.problem_formula10(list(r), [0.25] * n, 211.0)
+    dsg = mc.Design([p], alpha, np.zeros(len(alpha), dtype=np.int32), seed=1)
+    vals = torch.tensor(y, dtype=torch.float64, device="cuda")
+    sm, lam_used = dsg.smooth(vals, lam)
+    ref, lam_ref = O.tps_smooth(x, y, lam)
+    if lam < 0 and lam_used.item() != pytest.approx(lam_ref, rel=1e-9):
+        assert O.gcv_score(x, y, lam_used.item()) == pytest.approx(O.gcv_score(x, y, lam_ref), rel=1e-9)
+        ref, _ = O.tps_smooth(x, y, lam_used.item())
+    assert np.allclose(sm.cpu().numpy(), ref, rtol=0, atol=1e-9)
+    A, v, st = dsg.refine(vals, lam_used.item())
+    xs, fs, _ = O.refine(x, y, lam_used.item())
+    assert st[0] == 0
+    assert v[0] == pytest.approx(fs, abs=1e-8)
+    assert np.allclose(A[0, : n - 1] / 0.025, xs, atol=1e-4)
