@@ -496,7 +496,7 @@ int64_t mc_num_designs(const mc_ctx* c) { return c ? c->D : -1; }
 int32_t mc_num_problems(const mc_ctx* c) { return c ? c->n_probs : -1; }
 int32_t mc_words_per_draw(const mc_ctx* c) { return c ? words_per_draw(c->n, c->est, c->model) : -1; }
 int32_t mc_draw_dump_stride(const mc_ctx* c) { return c ? draw_dump_stride(c->n, c->est, c->model) : -1; }
-int64_t mc_kernel_launches(const mc_ctx* c) { return c ? c->launches : -1; }
+int64_t mc_kernel_launches(const mc_ctx* c) { return c ? c->launches.load() : (int64_t)-1; }
 
 mc_status mc_philox_dump(uint64_t seed, const uint32_t* design, const uint64_t* word, int64_t count, uint32_t* out,
                          void* stream) {

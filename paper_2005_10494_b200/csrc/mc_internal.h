@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -79,7 +80,7 @@ struct mc_ctx {
   int64_t* d_prob_begin = nullptr;       // [n_probs+1]
   int block_threads = 256;
   int grid_blocks = 0;                   // 0 = auto
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};       // atomic: the plan builder may run on another host thread
   bool plan_built = false;
   std::vector<mci::TpsPlan> plans;
   double* d_tps_scratch = nullptr;       // per-problem scratch for smoothing

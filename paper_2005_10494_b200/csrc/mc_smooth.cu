@@ -375,7 +375,11 @@ mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
     for (int t = 0; t < nl && s == MC_OK; ++t) {
       PlanLane& ln = lanes[t];
       cudaError_t e;
-      if ((e = cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking)) != cudaSuccess) { s = cuda_fail(e, "plan stream"); break; }
+      // highest priority: when the plan is built while the fused MC kernel runs (Design.smooth_plan(wait=False)),
+      // the plan's latency-bound cuSOLVER blocks are scheduled ahead of queued MC blocks
+      int prio_lo = 0, prio_hi = 0;
+      cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+      if ((e = cudaStreamCreateWithPriority(&ln.st, cudaStreamNonBlocking, prio_hi)) != cudaSuccess) { s = cuda_fail(e, "plan stream"); break; }
       if (cusolverDnCreate(&ln.h) != CUSOLVER_STATUS_SUCCESS) { set_error("cusolverDnCreate failed"); s = MC_ERR_CUDA; break; }
       cusolverDnSetStream(ln.h, ln.st);
       if ((e = cudaMalloc(&ln.K, sizeof(double) * Nmax * Nmax)) != cudaSuccess ||

@@ -241,6 +241,10 @@ class Design:
         self.n_probs = len(self.problems)
 
     def close(self):
+        try:
+            self._join_plan()
+        except McError:
+            pass
         if getattr(self, "_ctx", None) is not None and self._ctx.value:
             lib().mc_destroy(self._ctx)
             self._ctx = None
@@ -262,6 +266,7 @@ class Design:
     def upload(self, alpha_host, stream=None):
         """Replace the design table from host memory (H2D + device thresholds); alpha_host may be a
         pinned torch CPU tensor (async copy) or a numpy array."""
+        self._join_plan()
         if hasattr(alpha_host, "data_ptr"):
             ptr = ctypes.cast(alpha_host.data_ptr(), ctypes.POINTER(ctypes.c_double))
         else:
@@ -312,17 +317,48 @@ class Design:
                                  _stream(stream)))
         return mean, var
 
-    def smooth_plan(self, fit_mask=None, stream=None):
+    def smooth_plan(self, fit_mask=None, stream=None, wait: bool = True):
+        """Row a9 prep: the per-problem TPS eigenbasis (mc_smooth_plan).  wait=False builds it on a host
+        thread (its own high-priority CUDA streams) so that it overlaps the Monte-Carlo pass; every call
+        that needs the plan (smooth, tps_fit, refine, upload, close) joins it first."""
         m = None
         if fit_mask is not None:
             m = np.ascontiguousarray(fit_mask, dtype=np.uint8)
             assert m.size == self.D
-        _check(lib().mc_smooth_plan(self._ctx, None if m is None else m.ctypes.data_as(ctypes.c_void_p),
-                                    _stream(stream)))
+        self._join_plan()
         self._mask_ref = m
+        mp = None if m is None else m.ctypes.data_as(ctypes.c_void_p)
+        if wait:
+            _check(lib().mc_smooth_plan(self._ctx, mp, _stream(stream)))
+            return
+        import threading
+        torch = _torch()
+        # the caller's work so far (e.g. the design upload) is complete before the plan reads the table
+        torch.cuda.current_stream(self.device).synchronize()
+        ctx, dev = self._ctx, self.device
+        self._plan_status = None
+
+        def run():
+            torch.cuda.set_device(dev)
+            side = torch.cuda.Stream(device=dev)
+            self._plan_status = (lib().mc_smooth_plan(ctx, mp, ctypes.c_void_p(side.cuda_stream)),
+                                 lib().mc_last_error())
+
+        self._plan_thread = threading.Thread(target=run, daemon=True)
+        self._plan_thread.start()
+
+    def _join_plan(self):
+        t = getattr(self, "_plan_thread", None)
+        if t is not None:
+            t.join()
+            self._plan_thread = None
+            st, msg = self._plan_status
+            if st != 0:
+                raise McError(st, msg.decode() if isinstance(msg, bytes) else str(msg))
 
     def smooth(self, values, lam: float = -1.0, stream=None):
         """Row a9: TPS-smoothed values and the lambda used per problem."""
+        self._join_plan()
         torch = _torch()
         out = torch.empty_like(values)
         lam_used = torch.empty(self.n_probs, dtype=torch.float64, device=values.device)
@@ -331,6 +367,7 @@ class Design:
         return out, lam_used
 
     def tps_fit(self, values, lam: float = -1.0, stream=None):
+        self._join_plan()
         _check(lib().mc_tps_fit(self._ctx, values.data_ptr(), float(lam), _stream(stream)))
 
     def tps_eval(self, problem: int, x):
@@ -342,6 +379,7 @@ class Design:
 
     def refine(self, values, lam: float = -1.0, stream=None):
         """NEXT f1: per-problem continuous optimum on the TPS surface (alpha*, P~*, status)."""
+        self._join_plan()
         A = np.zeros((self.n_probs, self.n))
         v = np.zeros(self.n_probs)
         st = np.zeros(self.n_probs, dtype=np.int32)

@@ -186,3 +186,25 @@ def test_grid_smooth_rejects_bad_input(mc, torch):
         mc.grid_smooth(torch.zeros((1, 3), dtype=torch.float64, device="cuda"), [0.1], [0, 1, 2])
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         mc.grid_smooth(torch.zeros((4, 3), dtype=torch.float64), [0.1, 0.2, 0.3, 0.4], [0, 1, 2])
+
+
+def test_plan_built_during_mc_pass_is_identical(O, mc, torch):
+    """smooth_plan(wait=False) overlaps the plan with a running MC pass: sums, smoothed values and lambda
+    are bit-identical to the sequential order."""
+    spec, alpha, x, f, y = _noisy_surface(O, m=16, seed=2)
+    pod = np.zeros(len(alpha), dtype=np.int32)
+    outs = []
+    for wait in (True, False):
+        dsg = mc.Design([lib_problem(mc, spec)], alpha, pod, seed=5)
+        if wait:
+            dsg.smooth_plan()
+        sums = dsg.new_sums()
+        if not wait:
+            dsg.smooth_plan(wait=False)
+        dsg.evaluate(sums, 0, 3_000_000)
+        mean, _ = dsg.finalize(sums, 3_000_000)
+        sm, lam = dsg.smooth(mean, -1.0)
+        outs.append((sums.cpu().numpy(), sm.cpu().numpy(), lam.cpu().numpy()))
+        dsg.close()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
