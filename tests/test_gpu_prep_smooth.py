@@ -208,3 +208,32 @@ def test_plan_built_during_mc_pass_is_identical(O, mc, torch):
         dsg.close()
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+
+
+def test_batched_plan_matches_oracle(O, mc, torch):
+    """Problems with equal fitted-set sizes take the batched eigensolver (>= 4 per group): 6 C2 problems
+    with an N3 = 60 oracle subset of the m = 12 grid each; smoothed values and GCV lambda per problem against
+    the oracle."""
+    specs = W.c2_problems()[::97][:6]
+    probs, alpha, pod, xs = [], [], [], []
+    for k, sp in enumerate(specs):
+        A = O.candidates(sp.r, sp.alpha0, 12, 60, W.SEED + k)
+        probs.append(lib_problem(mc, sp))
+        alpha.append(A)
+        pod += [k] * len(A)
+        xs.append(A[:, :2] / sp.alpha0)
+    alpha = np.concatenate(alpha)
+    dsg = mc.Design(probs, alpha, np.array(pod, dtype=np.int32), seed=1)
+    rng = np.random.default_rng(9)
+    y = np.concatenate([0.9 + 0.05 * np.sin(2 * x[:, 0] + x[:, 1]) + 1e-3 * rng.normal(size=len(x)) for x in xs])
+    sm, lam = dsg.smooth(torch.tensor(y, dtype=torch.float64, device="cuda"), -1.0)
+    sm, lam = sm.cpu().numpy(), lam.cpu().numpy()
+    off = 0
+    for k, x in enumerate(xs):
+        yk = y[off:off + len(x)]
+        ref, lref = O.tps_smooth(x, yk, -1.0)
+        if lam[k] != pytest.approx(lref, rel=1e-9):
+            assert O.gcv_score(x, yk, lam[k]) == pytest.approx(O.gcv_score(x, yk, lref), rel=1e-9)
+            ref, _ = O.tps_smooth(x, yk, lam[k])
+        assert np.allclose(sm[off:off + len(x)], ref, rtol=0, atol=1e-9), k
+        off += len(x)
