@@ -223,66 +223,18 @@ __device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
   e = pos ? qc : qp;
 }
 
-// Standard normal quantile Phi^{-1}(p) given p and its complement pc = 1 - p (both computed
-// accurately by the caller), via erfinv(y) = g(w) y, y = 2p - 1 = p - pc, w = -ln(4 p pc):
-// central (w < 5) and near-tail (w < 16) polynomials of M. Giles, "Approximating the erfinv
-// function" (GPU Computing Gems Jade, 2011); deep tail (w >= 16, p < 1.1e-7) our own fit
-// (tools/fit_erfinv_deep_tail.py).  Relative error < 6e-7 for p in (1e-38, 1).
-__device__ __forceinline__ float normal_quantile(float p, float pc) {
-  const float pp = fmaxf(p * pc, 1.0e-38f);
-  const float w = -0.69314718056f * (lg2_approx(pp) + 2.0f);
-  float g;
-  if (w < 5.0f) {
-    const float ww = w - 2.5f;
-    g = 2.81022636e-08f;
-    g = fmaf(g, ww, 3.43273939e-07f);
-    g = fmaf(g, ww, -3.5233877e-06f);
-    g = fmaf(g, ww, -4.39150654e-06f);
-    g = fmaf(g, ww, 0.00021858087f);
-    g = fmaf(g, ww, -0.00125372503f);
-    g = fmaf(g, ww, -0.00417768164f);
-    g = fmaf(g, ww, 0.246640727f);
-    g = fmaf(g, ww, 1.50140941f);
-  } else {
-    const float sw = sqrt_approx(fminf(w, 88.0f));
-    if (w < 16.0f) {
-      const float ww = sw - 3.0f;
-      g = -0.000200214257f;
-      g = fmaf(g, ww, 0.000100950558f);
-      g = fmaf(g, ww, 0.00134934322f);
-      g = fmaf(g, ww, -0.00367342844f);
-      g = fmaf(g, ww, 0.00573950773f);
-      g = fmaf(g, ww, -0.0076224613f);
-      g = fmaf(g, ww, 0.00943887047f);
-      g = fmaf(g, ww, 1.00167406f);
-      g = fmaf(g, ww, 2.83297682f);
-    } else {
-      const float ww = sw - 6.0f;
-      g = 7.926354328446905e-07f;
-      g = fmaf(g, ww, -6.932396900083404e-06f);
-      g = fmaf(g, ww, 2.5214179913746193e-05f);
-      g = fmaf(g, ww, -3.964155257563107e-05f);
-      g = fmaf(g, ww, -0.0004801170143764466f);
-      g = fmaf(g, ww, 1.0096029043197632f);
-      g = fmaf(g, ww, 5.859915256500244f);
-    }
-  }
-  return 1.41421356237f * g * (p - pc);
-}
-
-// normal_quantile() with sqrt(2) folded into the polynomial coefficients (one FMUL less).
-#ifndef MC_QUANTILE_BRANCHFREE
-#define MC_QUANTILE_BRANCHFREE 1
-#endif
+// Standard normal quantile Phi^{-1}(p) given p and its complement pc = 1 - p (both computed accurately by
+// the caller), via erfinv(y) = g(w) y, y = 2p - 1 = p - pc, w = -ln(4 p pc), for w in [0, 16]
+// (p in [2.8e-8, 1 - 2.8e-8]): ONE degree-12 polynomial in sqrt(w + 2) (tools/fit_erfinv_single.py,
+// relative error 5.3e-7 in fp32; sqrt(2) folded into the coefficients) — no per-coefficient selects on
+// the ALU pipe and no branch.  Beyond that range the argument is clamped to w = 16 (reading R24): in the
+// SOV this only happens when v e_k < 2.8e-8 (the upper side cannot clamp: 1 - v >= 2^-24), and the
+// resulting change of u is at most e_k on an event of probability <= 2.8e-8 / e_k, i.e. a bias of at
+// most 2.8e-8 per even stage.  Replacing the deep-tail branch (BSSY/FSETP/BRA/BSYNC per call and warp
+// divergence) measured +4.8 % draws/s on C2 (profiles/r01/tune_grid.txt).
 __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
-  constexpr double S2 = 1.4142135623730950488;
-  // p pc may flush to 0 (e ~ 0): lg2 -> -inf, w -> +inf, handled by the deep-tail clamp
-#if MC_QUANTILE_BRANCHFREE
-  // w in [0, 16) (p in [1.1e-7, 1 - 1.1e-7]): ONE degree-12 polynomial in sqrt(w + 2)
-  // (tools/fit_erfinv_single.py, relative error 5.3e-7 in fp32) -- no per-coefficient selects on the
-  // ALU pipe; the deep tail w >= 16 (e_i < ~1e-7) takes a rare divergent branch.
-  // w + 2 = -ln2 lg2(p pc) + (2 - 2 ln2) in one FFMA.
-  const float w2 = fmaf(lg2_approx(p * pc), -0.69314718056f, 0.61370563888f);
+  // w + 2 = -ln2 lg2(p pc) + (2 - 2 ln2) in one FFMA; p pc may flush to 0 (lg2 -> -inf): the clamp holds
+  const float w2 = fminf(fmaf(lg2_approx(p * pc), -0.69314718056f, 0.61370563888f), 18.0f);
   const float x = sqrt_approx(w2) - 2.82842712474619f;
   float g = -0.0001458914359425521f;
   g = fmaf(g, x, 0.00014054195626482066f);
@@ -297,88 +249,6 @@ __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
   g = fmaf(g, x, -0.018363709814932894f);
   g = fmaf(g, x, 1.59782737417905f);
   g = fmaf(g, x, 3.2334928032079135f);
-  if (w2 >= 18.0f) {
-    const float ww = sqrt_approx(fminf(w2 - 2.0f, 88.0f)) - 6.0f;
-    g = (float)(7.926354328446905e-07 * S2);
-    g = fmaf(g, ww, (float)(-6.932396900083404e-06 * S2));
-    g = fmaf(g, ww, (float)(2.5214179913746193e-05 * S2));
-    g = fmaf(g, ww, (float)(-3.964155257563107e-05 * S2));
-    g = fmaf(g, ww, (float)(-0.0004801170143764466 * S2));
-    g = fmaf(g, ww, (float)(1.0096029043197632 * S2));
-    g = fmaf(g, ww, (float)(5.859915256500244 * S2));
-  }
-  return g * (p - pc);
-#else
-  const float w = -0.69314718056f * (lg2_approx(p * pc) + 2.0f);
-  float g;
-  if (w < 5.0f) {
-    const float ww = w - 2.5f;
-    g = (float)(2.81022636e-08 * S2);
-    g = fmaf(g, ww, (float)(3.43273939e-07 * S2));
-    g = fmaf(g, ww, (float)(-3.5233877e-06 * S2));
-    g = fmaf(g, ww, (float)(-4.39150654e-06 * S2));
-    g = fmaf(g, ww, (float)(0.00021858087 * S2));
-    g = fmaf(g, ww, (float)(-0.00125372503 * S2));
-    g = fmaf(g, ww, (float)(-0.00417768164 * S2));
-    g = fmaf(g, ww, (float)(0.246640727 * S2));
-    g = fmaf(g, ww, (float)(1.50140941 * S2));
-  } else {
-    const float sw = sqrt_approx(fminf(w, 88.0f));
-    if (w < 16.0f) {
-      const float ww = sw - 3.0f;
-      g = (float)(-0.000200214257 * S2);
-      g = fmaf(g, ww, (float)(0.000100950558 * S2));
-      g = fmaf(g, ww, (float)(0.00134934322 * S2));
-      g = fmaf(g, ww, (float)(-0.00367342844 * S2));
-      g = fmaf(g, ww, (float)(0.00573950773 * S2));
-      g = fmaf(g, ww, (float)(-0.0076224613 * S2));
-      g = fmaf(g, ww, (float)(0.00943887047 * S2));
-      g = fmaf(g, ww, (float)(1.00167406 * S2));
-      g = fmaf(g, ww, (float)(2.83297682 * S2));
-    } else {
-      const float ww = sw - 6.0f;
-      g = (float)(7.926354328446905e-07 * S2);
-      g = fmaf(g, ww, (float)(-6.932396900083404e-06 * S2));
-      g = fmaf(g, ww, (float)(2.5214179913746193e-05 * S2));
-      g = fmaf(g, ww, (float)(-3.964155257563107e-05 * S2));
-      g = fmaf(g, ww, (float)(-0.0004801170143764466 * S2));
-      g = fmaf(g, ww, (float)(1.0096029043197632 * S2));
-      g = fmaf(g, ww, (float)(5.859915256500244 * S2));
-    }
-  }
-  return g * (p - pc);
-#endif
-}
-
-// normal_quantile_fast split for batching: the main polynomial (valid for w < 16) and the deep tail.
-__device__ __forceinline__ float quantile_main(float p, float pc, float& w) {
-  w = -0.69314718056f * (lg2_approx(p * pc) + 2.0f);
-  const float x = sqrt_approx(w + 2.0f) - 2.82842712474619f;
-  float g = -0.0001458914359425521f;
-  g = fmaf(g, x, 0.00014054195626482066f);
-  g = fmaf(g, x, 0.0012376677239334937f);
-  g = fmaf(g, x, -0.0017637622021570974f);
-  g = fmaf(g, x, -0.0036462519812319317f);
-  g = fmaf(g, x, 0.009457966527136036f);
-  g = fmaf(g, x, -0.0013609513949184736f);
-  g = fmaf(g, x, -0.022852510105916587f);
-  g = fmaf(g, x, 0.04599717902636056f);
-  g = fmaf(g, x, -0.040789581299890895f);
-  g = fmaf(g, x, -0.018363709814932894f);
-  g = fmaf(g, x, 1.59782737417905f);
-  g = fmaf(g, x, 3.2334928032079135f);
-  return g * (p - pc);
-}
-__device__ __forceinline__ float quantile_deep(float p, float pc, float w) {
-  constexpr double S2 = 1.4142135623730950488;
-  const float ww = sqrt_approx(fminf(w, 88.0f)) - 6.0f;
-  float g = (float)(7.926354328446905e-07 * S2);
-  g = fmaf(g, ww, (float)(-6.932396900083404e-06 * S2));
-  g = fmaf(g, ww, (float)(2.5214179913746193e-05 * S2));
-  g = fmaf(g, ww, (float)(-3.964155257563107e-05 * S2));
-  g = fmaf(g, ww, (float)(-0.0004801170143764466 * S2));
-  g = fmaf(g, ww, (float)(1.0096029043197632 * S2));
-  g = fmaf(g, ww, (float)(5.859915256500244 * S2));
   return g * (p - pc);
 }
 

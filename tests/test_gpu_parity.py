@@ -479,3 +479,30 @@ def test_c3_scale_unbiased_against_exact_assurance(O, mc, torch, est):
     assert np.abs(z).max() < 5.0, np.abs(z).max()
     assert abs(z.mean()) < 5.0 / np.sqrt(len(z)), z.mean()
     assert 0.5 < (z * z).mean() < 1.6          # the reported SE is the right size
+
+
+def test_inverse_cdf_clamp_region(O, mc, torch):
+    """Reading R24: the kernel clamps the SOV inverse-CDF argument at w = 16 (v e_2 >= 2.8e-8).  With a
+    point-mass effect putting b_2 = -5.6 (e_2 = 1.1e-8 < 2.8e-8: EVERY draw clamps), u stays within the
+    bound |du| <= e_2 of the exact oracle, i.e. within fp32 resolution of u near 1."""
+    r = [1.0, 0.45, 0.15]
+    a = [0.004, 0.012, 0.0]
+    a[2] = O.solve_alpha_n(r, 0.025, a[:2], 1e-13)
+    i3 = 211.0
+    z2 = -O.Phi_inv(a[1])
+    th2 = (z2 + 5.6) / math.sqrt(r[1] * i3)
+    theta = [0.05, th2, 0.05]
+    p = mc.problem_point_mass(r, theta, i3)
+    dsg = mc.Design([p], [a], [0], seed=SEED, estimator=0)
+    S = np.arange(0, 4000, dtype=np.int64) * 7919 + 1
+    rec = dsg.draw_dump(torch.zeros(len(S), dtype=torch.int64).cuda(), torch.tensor(S).cuda()).cpu().numpy()
+    op = O.point_mass_problem(r, theta, i3)
+    for i, s in enumerate(S[:400]):
+        o = O.draw(op, a, 0, SEED, 0, int(s))
+        assert abs(float(rec[i, -1]) - o["u"]) <= 1.5e-7, (s, rec[i, -1], o["u"])
+    N = 400_000
+    sums = dsg.new_sums()
+    dsg.evaluate(sums, 0, N)
+    got = dsg.finalize(sums, N)[0].item()
+    ref = O.finalize(_oracle_sums(O, op, a, 0, 0, 0, N), N)[0][0]
+    assert abs(got - ref) <= 1e-6 * ref, (got, ref)

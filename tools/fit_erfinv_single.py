@@ -3,8 +3,7 @@ normal_quantile_fast): erfinv(y) = y * g(w), w = -ln(1 - y^2) = -ln(4 p (1-p)), 
 (p in [1.1e-7, 1 - 1.1e-7]), as ONE degree-12 polynomial in s = sqrt(w + 2) - (sqrt2 + sqrt18)/2,
 fitted by iteratively reweighted least squares towards the minimax relative error.  Replaces the
 central/tail pair of M. Giles' single-precision erfinv (two polynomials and a select per coefficient),
-which cost the ALU pipe ten FSELs per call.  The deep tail (w >= 16) keeps the separate fit of
-tools/fit_erfinv_deep_tail.py behind a (rare) branch.
+which cost the ALU pipe ten FSELs per call.  Beyond w = 16 the kernel clamps the argument (R24).
 
 Prints the coefficients (highest degree first, pre-multiplied by sqrt(2) so that
 Phi^{-1}(p) = g'(w) (p - (1 - p))) and the max relative error of an fp32 Horner evaluation.
