@@ -33,7 +33,7 @@ from paper_2005_10494_b200 import workloads as W  # noqa: E402
 # Per-draw issue slots of the fused kernel's steady-state loop (n = 3), counted from the sm_100a SASS
 # of the library being timed by tools/sass_count.py: the ALU/issue roofline's work per
 # draw.  The fallback constants are that tool's output for the committed kernel.
-ISSUE_PER_DRAW_FALLBACK = {"cond": 148.5, "ind": 108.0}
+ISSUE_PER_DRAW_FALLBACK = {"cond": 145.5, "ind": 108.0}
 
 
 def issue_per_draw(est: str) -> float:

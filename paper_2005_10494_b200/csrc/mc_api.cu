@@ -113,6 +113,8 @@ static mc_status validate_problem(const mc_problem& p, int idx) {
 }
 
 constexpr double BM_K = 1.17741002251547469;   // sqrt(2 ln 2), see mc_device.cuh
+constexpr double PHI_SCALE = 0.84932180028801904;   // sqrt(log2(e) / 2): COND carries every normal-CDF
+                                                     // argument pre-scaled by it (mc_device.cuh normal_tail)
 
 // COND stage coefficients of the SOV order (2, 4, ..., 1, 3, ...) for the Formula-1 Markov chain
 // (A.1): X_{j+1} = rho_j X_j + s_j W (0-based j).  Even populations (0-based p = 2k+1) form the chain
@@ -170,7 +172,7 @@ static SovCoef sov_coef(const mc_problem& p) {
 // Row scale of b folded into the record and the thresholds (mc_device.cuh ProbRegs).
 static double row_scale(const mc_problem& p, int est, int i) {
   if (est == MC_EST_IND) return 1.0 / BM_K;
-  return 1.0 / sov_coef(p).sd[i];
+  return PHI_SCALE / sov_coef(p).sd[i];
 }
 
 // Per-problem device record (fp32): M = diag(c) L_p packed with the folded scales, the IND Markov
@@ -207,13 +209,13 @@ static void problem_record(const mc_problem& p, int est, float* rec) {
     rec[OFF_SD + i] = (float)sd[i];
   }
   for (int k = 0; 2 * k + 1 < n; ++k) {
-    rec[OFF_ER + k] = (float)(sc.emu[k] / sc.esd[k]);
+    rec[OFF_ER + k] = (float)(PHI_SCALE * sc.emu[k] / sc.esd[k]);
     rec[OFF_EMU + k] = (float)sc.emu[k];
     rec[OFF_ESD + k] = (float)sc.esd[k];
   }
   for (int j = 0; 2 * j < n; ++j) {
-    rec[OFF_OA + j] = (float)(sc.oa[j] / sc.sd[2 * j]);
-    rec[OFF_OB + j] = (float)(sc.ob[j] / sc.sd[2 * j]);
+    rec[OFF_OA + j] = (float)(PHI_SCALE * sc.oa[j] / sc.sd[2 * j]);
+    rec[OFF_OB + j] = (float)(PHI_SCALE * sc.ob[j] / sc.sd[2 * j]);
   }
   if (p.model == 1) {
     // C4 strata prior: the kernel draws eps / BM_K, so every sd carries BM_K

@@ -202,10 +202,12 @@ __device__ __forceinline__ void box_muller_scaled(uint32_t wr, uint32_t wa, uint
 // t = 1/(1 + kappa a), q = t exp(-a^2/2 + poly(t))) refitted in base 2 with a degree-8 polynomial
 // (tools/fit_normal_tail.py: kappa = 0.4/sqrt2, max relative error 9.2e-8 in exact arithmetic): one RCP,
 // eight FFMAs, one EX2 on the MUFU pipe.  Returns q and e = 1 - q (= Phi(a)) without cancellation for
-// either sign of a.
+// either sign of a.  The argument arrives PRE-SCALED, a' = a sqrt(log2(e)/2) (the COND record folds the
+// factor into M, the thresholds and the stage coefficients: mc_api.cu PHI_SCALE), so the exponent
+// -a^2 log2(e)/2 = -a'^2 is one FFMA and kappa becomes kappa / sqrt(log2(e)/2).
 __device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
   const float aa = fabsf(a);
-  const float t = rcp_approx(fmaf(aa, 0.282842712474619f, 1.0f));
+  const float t = rcp_approx(fmaf(aa, (float)(0.28284271247461901 / 0.84932180028801904), 1.0f));
   float p = -0.3020209548193252f;
   p = fmaf(p, t, 1.3475361161107364f);
   p = fmaf(p, t, -2.173205689641004f);
@@ -215,7 +217,7 @@ __device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
   p = fmaf(p, t, 0.5735953408558541f);
   p = fmaf(p, t, 1.4456196577402736f);
   p = fmaf(p, t, -3.1477861996521375f);
-  const float ex = ex2_approx(fmaf(aa * aa, -0.72134752044448170f, p));   // -a^2 log2(e) / 2
+  const float ex = ex2_approx(fmaf(-aa, aa, p));   // -a'^2 = -a^2 log2(e) / 2
   const float qp = t * ex;                     // Phi(-|a|)
   const float qc = 1.0f - qp;                  // Phi(|a|)
   const bool pos = a >= 0.0f;
