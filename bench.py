@@ -279,7 +279,7 @@ def run_ours(args):
     achieved = ipd * draws_launch / (kms * 1e-3) / 1e12
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "Tinst/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "traffic_ncu": {"dram_bytes_per_launch": 453888, "draws_per_launch": 1.2e10,
+            "traffic_ncu": {"dram_bytes_per_launch": 448256, "draws_per_launch": 1.2e10,
                             "capture": "profiles/r01/ncu_fused_cond_summary.txt (--problems 6; the full C2 launch "
                                        "times out under --set full replay)",
                             "note": "DRAM bytes scale with designs (zc, problem_of_design, sums), not draws: "
