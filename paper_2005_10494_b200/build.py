@@ -32,15 +32,34 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file), then link the shared library."""
     if not force and not needs_build() and "MC_LIB_OUT" not in os.environ:
         return LIB
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
     out = os.environ.get("MC_LIB_OUT", LIB)
     extra = os.environ.get("MC_EXTRA_FLAGS", "").split()
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", out, *sources(), "-lcusolver", "-lcublas"]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+    with tempfile.TemporaryDirectory(prefix="mc_build_") as tmp:
+        objs, cmds = [], []
+        for src in sources():
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            cmd = [NVCC, *ARCH, *compile_flags, *extra, "-c", "-o", obj, src]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            objs.append(obj)
+            cmds.append(cmd)
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), file=sys.stderr)
+        with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+            results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+        for c, r in zip(cmds, results):
+            sys.stderr.write(r.stdout + r.stderr)
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, c)
+        link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out, *objs, "-lcusolver", "-lcublas"]
+        subprocess.check_call(link)
     return LIB
 
 
