@@ -34,16 +34,25 @@ from paper_2005_10494_b200 import workloads as W  # noqa: E402
 # of the library being timed by tools/sass_count.py: the ALU/issue roofline's work per
 # draw.  The fallback constants are that tool's output for the committed kernel.
 ISSUE_PER_DRAW_FALLBACK = {"cond": 145.5, "ind": 108.0}
+PIPE_MIX_FALLBACK = {"cond": {"issue": 145.5, "fp32": 78.5, "sfu": 14.0, "imad_wide": 18.0},
+                     "ind": {"issue": 108.0, "fp32": 26.0, "sfu": 12.0, "imad_wide": 27.0}}
 
 
-def issue_per_draw(est: str) -> float:
+def pipe_mix(est: str) -> dict:
+    """Per-draw issue slots, FP32 and SFU instructions of the timed kernel's executed common path, counted
+    from the SASS of the library being timed (tools/sass_count.py); the last measured values if cuobjdump
+    is unavailable."""
     try:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import sass_count
         from paper_2005_10494_b200 import build
-        return float(sass_count.issue_per_draw(3, 0 if est == "cond" else 1, build.LIB))
+        return sass_count.pipe_mix(3, 0 if est == "cond" else 1, build.LIB)
     except Exception:
-        return ISSUE_PER_DRAW_FALLBACK[est]
+        return dict(PIPE_MIX_FALLBACK[est])
+
+
+def issue_per_draw(est: str) -> float:
+    return float(pipe_mix(est)["issue"])
 
 
 ISSUE_LANES_PER_CLK_PER_SM = 128           # 4 SMSPs x 32 lanes, one warp-instruction per SMSP per clock
@@ -275,8 +284,20 @@ def run_ours(args):
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     mhz = clk.get("sm_mhz") or 1965.0
     peak = ISSUE_LANES_PER_CLK_PER_SM * sm_count * (clk.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12   # T lane-instr/s
-    ipd = issue_per_draw(args.est) if not args.crn else float("nan")
+    mix = pipe_mix(args.est)
+    ipd = mix["issue"] if not args.crn else float("nan")
     achieved = ipd * draws_launch / (kms * 1e-3) / 1e12
+    rate = draws_launch / (kms * 1e-3)
+    fmax = (clk.get("sm_max_mhz") or 1965.0) * 1e6
+    # the north star's "fraction of the FP32/SFU roofline": per-pipe achieved lane-op rates against the
+    # pipe peaks (FP32 128 and MUFU 16 lane-ops/clk/SM, profiles/r01/pipes.json)
+    pipes = None if args.crn else {
+        "fp32": {"per_draw": mix["fp32"], "achieved": round(mix["fp32"] * rate / 1e12, 3),
+                 "peak": round(128 * sm_count * fmax / 1e12, 3), "unit": "T lane-op/s",
+                 "frac": round(mix["fp32"] * rate / (128 * sm_count * fmax), 4)},
+        "sfu": {"per_draw": mix["sfu"], "achieved": round(mix["sfu"] * rate / 1e12, 3),
+                "peak": round(16 * sm_count * fmax / 1e12, 3), "unit": "T lane-op/s",
+                "frac": round(mix["sfu"] * rate / (16 * sm_count * fmax), 4)}}
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "Tinst/s",
             "frac": round(achieved / peak, 4), "traffic": None,
             "traffic_ncu": {"dram_bytes_per_launch": 448256, "draws_per_launch": 1.2e10,
@@ -288,6 +309,7 @@ def run_ours(args):
             "kernel_ms": round(kms, 3),
             "kernel_share_of_step": round(kms / (ms / args.steps), 4),
             "issue_per_draw": ipd,
+            "pipes": pipes,
             "peak_basis": "128 lane-instr/clk/SM x SMs x sm_max_mhz (DESIGN.md §4)",
             "draws_per_s_kernel": draws_launch / (kms * 1e-3) * world}
 

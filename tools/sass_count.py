@@ -114,6 +114,23 @@ def issue_per_draw(n: int = 3, est: int = 0, lib: str = None) -> float:
     return len(steady_loop(sass(n, est, lib))) / draws_per_iter(n, est)
 
 
+FP32_OPS = ("FFMA", "FMUL", "FADD")       # the FP32 (FMA) pipe's arithmetic
+SFU_OPS = ("MUFU",)
+
+
+def pipe_mix(n: int = 3, est: int = 0, lib: str = None) -> dict:
+    """Per-draw counts of the executed common path by pipe class: issue slots, FP32 (FFMA/FMUL/FADD),
+    SFU (MUFU) and IMAD.WIDE (the Philox multiplies)."""
+    path = steady_loop(sass(n, est, lib))
+    L = draws_per_iter(n, est)
+    ops = [(t.split()[1] if t.startswith("@") else t.split()[0]) for _, t in path]
+    base = [o.split(".")[0] for o in ops]
+    return {"issue": len(path) / L,
+            "fp32": sum(b in FP32_OPS for b in base) / L,
+            "sfu": sum(b in SFU_OPS for b in base) / L,
+            "imad_wide": sum(o.startswith("IMAD.WIDE") for o in ops) / L}
+
+
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     est = int(sys.argv[2]) if len(sys.argv) > 2 else 0
