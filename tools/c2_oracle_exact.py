@@ -39,8 +39,13 @@ def main():
     ap.add_argument("--every", type=int, default=16)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "c2_exact_sample.json"))
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 4)
+    ap.add_argument("--max-r2", type=float, default=0.7,
+                    help="skip problems with r2 above this (the oracle's FWER quadrature needs ~1 h per problem "
+                         "of 4096 bisection solves as rho -> 1)")
     a = ap.parse_args()
-    ks = list(range(0, 513, a.every))
+    from paper_2005_10494_b200 import workloads as W
+    specs = W.c2_problems()
+    ks = [k for k in range(0, 513, a.every) if specs[k].r[1] <= a.max_r2]
     with Pool(a.procs) as pool:
         rows = pool.map(one, ks)
     np.savez_compressed(a.out.replace(".json", ".npz"), **{f"P{r['problem']}": r.pop("P") for r in rows})
