@@ -3,9 +3,11 @@ the 513 C2 problems, the oracle's own candidate designs (m = 64 grid, alpha_3 by
 N3 = 2000 subset with seed + problem index) and the exact Formula-4 value of every design
 (Gaussian collapse + Markov orthant quadrature), its exact argmax and the top-2 gap.
 
-    python tools/c2_oracle_exact.py --every 16 --out profiles/r01/c2_exact_sample.json
+    python tests/golden/make_c2_exact_sample.py --every 16 --max-r2 0.7
 
-Test infrastructure (reads oracle/ only; the GPU result is compared afterwards by tools/c2_compare.py).
+Test infrastructure: a committed script that calls only oracle/ (and the input generators) and writes the
+stored expected values tests/golden/c2_exact_sample.{json,npz}; the GPU result of tools/c2_full_run.py is
+compared with them by tools/c2_compare.py.
 """
 import argparse
 import json
@@ -15,7 +17,7 @@ from multiprocessing import Pool
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 
@@ -37,7 +39,7 @@ def one(k):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--every", type=int, default=16)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "c2_exact_sample.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "c2_exact_sample.json"))
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 4)
     ap.add_argument("--max-r2", type=float, default=0.7,
                     help="skip problems with r2 above this (the oracle's FWER quadrature needs ~1 h per problem "
@@ -50,7 +52,7 @@ def main():
         rows = pool.map(one, ks)
     np.savez_compressed(a.out.replace(".json", ".npz"), **{f"P{r['problem']}": r.pop("P") for r in rows})
     with open(a.out, "w") as f:
-        json.dump({"source": "oracle only (tools/c2_oracle_exact.py)", "problems": rows}, f, indent=1)
+        json.dump({"source": "oracle only (tests/golden/make_c2_exact_sample.py)", "problems": rows}, f, indent=1)
     print(len(rows), "problems ->", a.out)
 
 

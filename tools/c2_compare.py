@@ -1,7 +1,7 @@
 """Compare the full-grid GPU run (tools/c2_full_run.py) with the oracle's exact reference
-(tools/c2_oracle_exact.py) on the sampled problems.
+(tests/golden/make_c2_exact_sample.py, oracle only) on the sampled problems.  Reads JSON/npz files only.
 
-    python tools/c2_compare.py gpurun_out/c2_1e9.json profiles/r01/c2_exact_sample.json > profiles/r01/c2_1e9_compare.json
+    python tools/c2_compare.py gpurun_out/c2_1e9.json tests/golden/c2_exact_sample.json > profiles/r01/c2_1e9_compare.json
 
 Per sampled problem: the GPU's raw-MC argmax (design index within the problem's N3 subset — the same
 designs on both sides: the alpha grid, alpha_3 and the subset are bit-/1e-11-identical)
