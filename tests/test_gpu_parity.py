@@ -506,3 +506,31 @@ def test_inverse_cdf_clamp_region(O, mc, torch):
     got = dsg.finalize(sums, N)[0].item()
     ref = O.finalize(_oracle_sums(O, op, a, 0, 0, 0, N), N)[0][0]
     assert abs(got - ref) <= 1e-6 * ref, (got, ref)
+
+
+def test_c5_mc_vs_quadrature_at_equal_budget(O, mc, torch):
+    """BASELINE configs[4] / SURVEY §8(d) C5: at a fixed budget the midpoint tensor-grid quadrature of
+    Formula 4 over the n-D prior (tests/golden/c5_quadrature.json, oracle only: m = floor(4096^(1/n)) nodes
+    per axis) degrades with n, while the MC estimate with the same number of draws keeps an n-independent
+    standard error and stays unbiased against the exact value."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c5_quadrature.json")))
+    rows = {r["n"]: r for r in g["rows"]}
+    ses = {}
+    for n, row in rows.items():
+        spec = W.c5_problem(n)
+        dsg = mc.Design([lib_problem(mc, spec)], np.array([row["alpha"]]), [0], seed=SEED, estimator=0)
+        B = row["nodes"]
+        sums = dsg.new_sums()
+        dsg.evaluate(sums, 0, B)
+        m, v = dsg.finalize(sums, B)
+        ses[n] = math.sqrt(v.item() / B)
+        assert abs(m.item() - row["exact"]) < 5 * ses[n] + 1e-6, (n, m.item(), row["exact"], ses[n])
+        if n >= 5:
+            assert row["abs_error"] > 10 * ses[n], (n, row["abs_error"], ses[n])   # MC wins in high dimension
+    assert rows[4]["abs_error"] > 100 * rows[3]["abs_error"]                       # quadrature error grows with n
+    # MC standard error per draw is dimension-free (same budget -> SE within a factor 3 over n = 3..10,
+    # after rescaling to a common number of draws)
+    per_draw = {n: ses[n] * math.sqrt(rows[n]["nodes"]) for n in ses}
+    assert max(per_draw.values()) < 3 * min(per_draw.values()), per_draw
