@@ -25,6 +25,7 @@ def main():
         r = gp[k]
         Pk = P[f"P{k}"]
         gi = r["raw_argmax_local"]
+        si = r["smoothed_argmax_local"]
         z = (r["P_hat"] - Pk[gi]) / r["SE"]
         ok_same = gi == e["exact_argmax_local"]
         ok_eps = Pk[gi] >= e["exact_max"] - 5 * r["SE"]
@@ -33,12 +34,19 @@ def main():
         rows.append({"problem": k, "scenario": e["scenario"], "r": e["r"], "gpu_argmax": gi,
                      "exact_argmax": e["exact_argmax_local"], "same": bool(ok_same),
                      "exact_gap12": e["gap12"], "SE": r["SE"], "P_exact_at_gpu": float(Pk[gi]),
-                     "exact_max": e["exact_max"], "within_5SE": bool(ok_eps), "z_at_gpu_design": float(z)})
+                     "exact_max": e["exact_max"], "within_5SE": bool(ok_eps), "z_at_gpu_design": float(z),
+                     "smoothed_argmax": si, "smoothed_same": bool(si == e["exact_argmax_local"]),
+                     "exact_loss_smoothed": float(e["exact_max"] - Pk[si])})
     zs = np.array([x["z_at_gpu_design"] for x in rows])
+    loss_raw = np.array([x["exact_max"] - x["P_exact_at_gpu"] for x in rows])
+    loss_sm = np.array([x["exact_loss_smoothed"] for x in rows])
     out = {"draws_per_design": g["draws_per_design"], "designs": g["designs"], "kernel_s": g["kernel_s"],
            "draws_per_s": g["draws_per_s"], "sampled_problems": len(rows), "argmax_identical": int(same),
            "argmax_within_5SE_of_exact_max": int(within),
            "z_at_gpu_designs": {"mean": float(zs.mean()), "max_abs": float(np.abs(zs).max())},
+           "exact_loss_raw_argmax": {"mean": float(loss_raw.mean()), "max": float(loss_raw.max())},
+           "smoothed_argmax_identical": int(sum(x["smoothed_same"] for x in rows)),
+           "exact_loss_smoothed_argmax": {"mean": float(loss_sm.mean()), "max": float(loss_sm.max())},
            "note": "the argmax of a noisy estimate is biased upward: z at the chosen design is positive on "
                    "average (winner's curse); identity is expected only where the exact top-2 gap >> SE",
            "rows": rows}
