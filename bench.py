@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work of the cpu_baseline sample")
     ap.add_argument("--no-tto-c2", action="store_true", help="skip the C2 time-to-optimal-design bookkeeping")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 dense-grid (strata prior) optimum")
+    ap.add_argument("--no-n4", action="store_true", help="skip the n = 4 problem (N3 = 4000, d = 3 TPS)")
     ap.add_argument("--tto-draws", type=int, default=W.DRAWS["C3"],
                     help="draws/design of the time-to-optimal-design run (C3 slice); 0 = skip")
     return ap.parse_args()
@@ -340,6 +341,9 @@ def run_ours(args):
     c4 = None
     if not args.no_c4:
         c4 = c4_optimal_design(mc, torch, dist, world, rank, local, est)
+    n4 = None
+    if not args.no_n4:
+        n4 = n4_optimal_design(mc, torch, dist, world, rank, local, est)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -359,7 +363,7 @@ def run_ours(args):
                                8.0 * sum((pod == k).sum() ** 2 for k in range(len(specs))) / 1e9)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "time_to_optimal_design": tto, "time_to_optimal_design_c2": tto_c2,
-                "c4_optimal_design": c4,
+                "c4_optimal_design": c4, "n4_optimal_design": n4,
                 "paper_literal_crossed_problem": paper_crossed,
                 "clocks": clk,
                 "prep_s": {"candidates": round(t_cand, 3), "tps_plan": round(t_plan, 3)},
@@ -395,6 +399,35 @@ def time_to_optimal_design(args, mc, torch, dist, world, rank, local, est):
            "designs": int(dsg.D), "draws_per_design": int(args.tto_draws), "n_gpus": world,
            "best_design": int(best), "best_alpha": [float(x) for x in alpha[best]], "P_smoothed": float(val),
            "P_hat": float(raw[best]), "SE": float(se[best]), "raw_argmax": int(np.argmax(raw)),
+           "lambda": float(res.lam_used.cpu().numpy()[0])}
+    dsg.close()
+    return out
+
+
+def n4_optimal_design(mc, torch, dist, world, rank, local, est):
+    """The paper's n = 4 workload (N3 = 4000 designs, a 3-D TPS): one problem from the statement to
+    the continuous optimum — candidates (m = 32 grid over alpha_1..3, alpha_4 solved on the GPU, seeded
+    N3 subset) -> MC (1e6 draws/design) -> all_reduce -> finalize -> TPS plan (N = 4000) + GCV -> argmax
+    -> L-BFGS on the 3-D TPS (f1)."""
+    spec = W.n4_problem()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prob = mc.problem_formula10(spec.r, spec.delta0(), spec.i3, spec.alpha0)
+    alpha, pod = mc.candidates([prob], m=W.N4_GRID_M, n3=W.N4_N3, seed=W.SEED, device=local)
+    dsg = mc.Design([prob], alpha, pod, seed=W.SEED, estimator=est, device=local)
+    res = mc.evaluate_design_objective(dsg, W.DRAWS["C2"], lam=-1.0, rank=rank, world=world)
+    best, val = res.best
+    A, v, st = dsg.refine(res.mean, -1.0)
+    t1 = time.perf_counter()
+    tt = torch.tensor([t1 - t0], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    out = {"seconds": float(tt[0]), "workload": "n = 4, r = (1, 0.6, 0.35, 0.15), scenario (c), N3 = 4000 of the "
+           "m = 32 grid, 1e6 draws/design", "designs": int(dsg.D), "best_design": int(best),
+           "best_alpha": [float(x) for x in alpha[best]], "P_smoothed": float(val),
+           "alpha_opt": [float(x) for x in A[0]], "P_opt": float(v[0]), "refine_status": int(st[0]),
            "lambda": float(res.lam_used.cpu().numpy()[0])}
     dsg.close()
     return out

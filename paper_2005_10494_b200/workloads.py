@@ -66,6 +66,16 @@ def c5_problem(n: int):
     return ProblemSpec(r=tuple((n - i) / n for i in range(n)), scenario="c", i3=211.0)
 
 
+def n4_problem():
+    """The paper's n = 4 workload (N3 = 4000, d = 3 TPS): scenario (c) law, I3 = 211, nested
+    fractions r = (1, 0.6, 0.35, 0.15) (the paper does not print its n = 4 r; these are a lattice point)."""
+    return ProblemSpec(r=(1.0, 0.6, 0.35, 0.15), scenario="c", i3=211.0)
+
+
+N4_GRID_M = 32      # m^3 = 32768 grid points over (alpha_1, alpha_2, alpha_3), alpha_4 solved
+N4_N3 = 4000        # P:388
+
+
 # draws per design (BASELINE.json configs)
 DRAWS = {"C1": 10_000, "C2": 1_000_000, "C3": 1_000_000_000, "C4": 1_000_000, "C5": 1_000_000}
 
