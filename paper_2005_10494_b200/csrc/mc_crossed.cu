@@ -36,26 +36,6 @@ __device__ __forceinline__ void load_problem_x(const float* __restrict__ rec, Pr
   }
 }
 
-// cnt += 1[exists i: x_i > b_i] (Formula 7's indicator, complemented) as one predicate chain
-template <int N>
-__device__ __forceinline__ void pair_count(const float* x, const float* b, float& cnt) {
-  if constexpr (N == 1) {
-    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; @p add.f32 %0, %0, 0f3F800000; }"
-        : "+f"(cnt) : "f"(x[0]), "f"(b[0]));
-  } else if constexpr (N == 2) {
-    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p; @p add.f32 %0, %0, 0f3F800000; }"
-        : "+f"(cnt) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]));
-  } else if constexpr (N == 3) {
-    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p; setp.gt.or.f32 p, %5, %6, p;"
-        " @p add.f32 %0, %0, 0f3F800000; }"
-        : "+f"(cnt) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]), "f"(x[2]), "f"(b[2]));
-  } else {
-    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p; setp.gt.or.f32 p, %5, %6, p;"
-        " setp.gt.or.f32 p, %7, %8, p; @p add.f32 %0, %0, 0f3F800000; }"
-        : "+f"(cnt) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]), "f"(x[2]), "f"(b[2]), "f"(x[3]), "f"(b[3]));
-  }
-}
-
 template <int N>
 __global__ void __launch_bounds__(XO_THREADS) k_crossed(const float* __restrict__ prob, const float* __restrict__ zc_all,
                                                         const int32_t* __restrict__ pod, uint64_t seed, uint64_t n1,
@@ -129,7 +109,7 @@ __global__ void __launch_bounds__(XO_THREADS) k_crossed(const float* __restrict_
 #pragma unroll
       for (int i = 0; i < N; ++i) x[i] = xs[t][i];
 #pragma unroll
-      for (int j = 0; j < XO_KO; ++j) pair_count<N>(x, bo[j], cf[j]);
+      for (int j = 0; j < XO_KO; ++j) ind_count<N>(x, bo[j], cf[j]);
     }
 #pragma unroll
     for (int j = 0; j < XO_KO; ++j) cnt[j] += (uint32_t)cf[j];

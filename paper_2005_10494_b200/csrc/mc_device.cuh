@@ -384,6 +384,27 @@ __device__ __forceinline__ float ind_indicator(const float* x, const float* b) {
   return u;
 }
 
+// cnt += 1[exists i: x_i > b_i] (the IND / Formula 7 rejection indicator) as ONE predicate chain (FSETP,
+// FSETP.OR ...) on the ALU pipe and one predicated FADD on the FMA pipe (the crossed and CRN kernels)
+template <int N>
+__device__ __forceinline__ void ind_count(const float* x, const float* b, float& cnt) {
+  if constexpr (N == 1) {
+    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; @p add.f32 %0, %0, 0f3F800000; }"
+        : "+f"(cnt) : "f"(x[0]), "f"(b[0]));
+  } else if constexpr (N == 2) {
+    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p; @p add.f32 %0, %0, 0f3F800000; }"
+        : "+f"(cnt) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]));
+  } else if constexpr (N == 3) {
+    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p; setp.gt.or.f32 p, %5, %6, p;"
+        " @p add.f32 %0, %0, 0f3F800000; }"
+        : "+f"(cnt) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]), "f"(x[2]), "f"(b[2]));
+  } else {
+    asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; setp.gt.or.f32 p, %3, %4, p; setp.gt.or.f32 p, %5, %6, p;"
+        " setp.gt.or.f32 p, %7, %8, p; @p add.f32 %0, %0, 0f3F800000; }"
+        : "+f"(cnt) : "f"(x[0]), "f"(b[0]), "f"(x[1]), "f"(b[1]), "f"(x[2]), "f"(b[2]), "f"(x[3]), "f"(b[3]));
+  }
+}
+
 // The design-dependent part: the utility u in [0, 1] from the thresholds b (= zc - v).
 template <int N, int EST, int MODEL>
 __device__ __forceinline__ float utility_of_b(const float* b, const Shared<N, EST, MODEL>& sh, const ProbRegs<N>& pr) {

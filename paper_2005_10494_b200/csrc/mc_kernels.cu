@@ -202,18 +202,18 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused
 // independent part of a draw (Philox, Box-Muller, the prior term, the IND null vector, the SOV
 // uniforms) is computed once and reused for a block of CRN_KD designs held in registers.
 // designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 4 / 2,
-// IND 16 / 4
+// IND 32 / 1 (IND: one shared y = X + v per sample, 3 compares + 1 predicated FADD per design: 2.74e12/s)
 #ifndef MC_CRN_KD_COND
 #define MC_CRN_KD_COND 4
 #endif
 #ifndef MC_CRN_KD_IND
-#define MC_CRN_KD_IND 16
+#define MC_CRN_KD_IND 32
 #endif
 #ifndef MC_CRN_MINB_COND
 #define MC_CRN_MINB_COND 2
 #endif
 #ifndef MC_CRN_MINB_IND
-#define MC_CRN_MINB_IND 4
+#define MC_CRN_MINB_IND 1
 #endif
 template <int EST> constexpr int crn_kd() { return EST == 0 ? MC_CRN_KD_COND : MC_CRN_KD_IND; }
 
@@ -227,6 +227,9 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
   const uint32_t lo1d = 0xCD9E8D57u * pid, hi1d = __umulhi(0xCD9E8D57u, pid);
   uint64_t q = G::word_of(s_begin) / 4;
   const uint32_t k1r1 = rk.k1[0] ^ 1u;   // counter word 3 = tag 1
+  float cf[EST == 1 ? KD : 1];            // IND steady state: fp32 counts per design
+#pragma unroll
+  for (int k = 0; k < (EST == 1 ? KD : 1); ++k) cf[k] = 0.0f;
 #pragma unroll 1
   for (int st = 0; st < STEPS; ++st) {
     const uint64_t s0 = s_begin + (uint64_t)st * G::L;
@@ -252,6 +255,16 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
           const uint64_t s = s0 + r * G::R + h;
           valid = s >= B && s < E;
         }
+        if constexpr (EST == 1 && !MASKED && MODEL == 0) {
+          // IND, steady state: X_i > zc_i - v_i  <=>  X_i + v_i > zc_i; y = X + v is shared by the KD designs,
+          // so each (design, sample) costs n compares in one predicate chain and one predicated FADD
+          float y[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) y[i] = sh.x[i] + sh.v[i];
+#pragma unroll
+          for (int k = 0; k < KD; ++k) ind_count<N>(y, zc[k], cf[k]);
+          continue;
+        }
 #pragma unroll
         for (int k = 0; k < KD; ++k) {
           float b[N];
@@ -264,6 +277,9 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
       }
     }
   }
+  if constexpr (EST == 1 && !MASKED && MODEL == 0)
+#pragma unroll
+    for (int k = 0; k < KD; ++k) a1[k] += (uint32_t)cf[k] << 23;   // counts <= 128: exact in fp32
   if constexpr (EST == 1)
 #pragma unroll
     for (int k = 0; k < KD; ++k) a2[k] = a1[k];
