@@ -133,7 +133,7 @@ mc_status mc_design_upload(mc_ctx* ctx, const double* alpha_host, void* cuda_str
 /* Sampling mode (NEXT f3): 0 = independent draws per design (stream keyed (design, sample), tag 0;
  * the default, reading R2); 1 = common random numbers per problem (stream keyed (problem, sample),
  * counter word 3 = 1): every design of a problem sees the same draws, so design differences have far
- * less noise and the draw's design-independent work is shared by blocks of designs (4 COND, 32 IND).
+ * less noise and the draw's design-independent work is shared by blocks of designs (12 COND, 32 IND).
  * n <= 3. */
 mc_status mc_set_sampling(mc_ctx* ctx, int32_t mode);
 

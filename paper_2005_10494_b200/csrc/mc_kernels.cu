@@ -201,16 +201,16 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused
 // (q_lo, q_hi, problem, 1)); every design of the problem sees the same draws, so the design-
 // independent part of a draw (Philox, Box-Muller, the prior term, the IND null vector, the SOV
 // uniforms) is computed once and reused for a block of CRN_KD designs held in registers.
-// designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 4 / 2,
+// designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 12 / 1 (3.34e11/s; 4 / 2 gave 2.98e11),
 // IND 32 / 1 (IND: one shared y = X + v per sample, 3 compares + 1 predicated FADD per design: 2.74e12/s)
 #ifndef MC_CRN_KD_COND
-#define MC_CRN_KD_COND 4
+#define MC_CRN_KD_COND 12
 #endif
 #ifndef MC_CRN_KD_IND
 #define MC_CRN_KD_IND 32
 #endif
 #ifndef MC_CRN_MINB_COND
-#define MC_CRN_MINB_COND 2
+#define MC_CRN_MINB_COND 1
 #endif
 #ifndef MC_CRN_MINB_IND
 #define MC_CRN_MINB_IND 1
