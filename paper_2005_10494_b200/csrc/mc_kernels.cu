@@ -150,9 +150,12 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
 
 // Work unit = one WARP tile: (design, 32 x SAMPLES_PER_THREAD consecutive samples).  Warps are
 // independent (no block barrier): each reduces its tile with 64-bit shuffles and lane 0 issues one
-// 64-bit atomicAdd pair.  Warp tiles are strided over the persistent grid's warps.
+// 64-bit atomicAdd pair.  Default launch: one tile per warp (a grid_blocks > 0 launch strides over the tiles).
+#ifndef MC_MIN_BLOCKS_C4
+#define MC_MIN_BLOCKS_C4 2
+#endif
 constexpr int min_blocks(int n, int est, int model) {
-  return model == 1 ? 2 : (n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1));
+  return model == 1 ? MC_MIN_BLOCKS_C4 : (n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1));
 }
 
 template <int N, int EST, int MODEL>

@@ -20,14 +20,20 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--draws", type=int, default=1_000_000)
     ap.add_argument("--crn", action="store_true")
+    ap.add_argument("--c4", action="store_true", help="time the C4 strata-prior kernel (model 1)")
     ap.add_argument("--crossed", type=str, default="", help="N1,N2: time the crossed estimator (IND ctx)")
     a = ap.parse_args()
     import torch
     from paper_2005_10494_b200 import mc
     from paper_2005_10494_b200 import workloads as W
-    specs = W.c2_problems()[:: max(1, 513 // a.problems)][: a.problems]
-    probs = [mc.problem_formula10(s.r, s.delta0(), s.i3, s.alpha0) for s in specs]
-    alpha, pod = mc.candidates(probs, m=W.GRID_M, n3=W.N3, seed=W.SEED)
+    if a.c4:
+        # C4 strata prior: 16 cutoffs x the 256-point alpha_1 grid
+        probs = [mc.problem_strata(r2, 211.0, W.C4_STRATA) for r2 in W.c4_r2_values()[::16]]
+        alpha, pod = mc.candidates(probs, m=W.C4_GRID, n3=0, seed=W.SEED)
+    else:
+        specs = W.c2_problems()[:: max(1, 513 // a.problems)][: a.problems]
+        probs = [mc.problem_formula10(s.r, s.delta0(), s.i3, s.alpha0) for s in specs]
+        alpha, pod = mc.candidates(probs, m=W.GRID_M, n3=W.N3, seed=W.SEED)
     dsg = mc.Design(probs, alpha, pod, seed=W.SEED, estimator=0 if a.est == "cond" else 1)
     dsg.set_launch(a.threads, a.grid)
     if a.crn:
