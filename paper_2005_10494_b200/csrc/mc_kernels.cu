@@ -1,8 +1,8 @@
 // mc_kernels.cu — K1 fused Monte-Carlo kernel, K2 finalize, K3 Philox dump, draw dump, K6 argmax.
 //
-// K1 (rows a2-a6 of DESIGN.md §1): persistent grid over warp tiles (design, 32 x 128 samples).
+// K1 (rows a2-a6 of DESIGN.md §1): one warp per warp tile (design, 32 x 128 samples), hardware-balanced.
 // Each thread owns 128 consecutive samples of one design, generates their Philox words in
-// registers (U words per draw, L draws per aligned step), evaluates u, and accumulates the exact
+// registers (records of R samples, WR words, LR records per aligned step), evaluates u, and accumulates the exact
 // 2^-23 fixed-point sums in 32-bit registers; a 64-bit warp shuffle reduction then issues one 64-bit
 // atomicAdd pair per warp tile (no block barrier).  Integer sums make the result independent of the
 // launch shape.
