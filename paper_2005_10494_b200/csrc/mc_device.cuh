@@ -157,10 +157,9 @@ __device__ __forceinline__ float sqrt_approx(float x) { float y; asm("sqrt.appro
 __device__ __forceinline__ float sin_approx(float x) { float y; asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float cos_approx(float x) { float y; asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
-// 1 + k 2^-23 in [1, 2) from the low 23 bits k of a Philox word: DESIGN.md §2.3.
-__device__ __forceinline__ float word_to_f12(uint32_t w) { return __uint_as_float((w & 0x007FFFFFu) | 0x3F800000u); }
-// Same as one LOP3 ((w & 0x7FFFFF) | one): `one` = 0x3F800000 held in a register by the caller
-// (ptxas cannot encode two immediates in one LOP3).
+// 1 + k 2^-23 in [1, 2) from the low 23 bits k of a Philox word as ONE LOP3
+// ((w & 0x7FFFFF) | one): `one` = 0x3F800000 held in a register by the caller (ptxas cannot encode two
+// immediates in one LOP3).
 __device__ __forceinline__ float word_to_f12(uint32_t w, uint32_t one) {
   uint32_t r;
   asm("lop3.b32 %0, %1, 0x007FFFFF, %2, 0xEA;" : "=r"(r) : "r"(w), "r"(one));
@@ -175,18 +174,6 @@ __device__ __forceinline__ uint32_t one_bits_reg() {
 // Box-Muller scale: R = sqrt(-2 ln u) = BM_K sqrt(-log2 u), BM_K = sqrt(2 ln 2).  The kernel draws the
 // scaled normals eps / BM_K and folds BM_K into the per-problem factors (see problem_record()).
 constexpr float BM_K = 1.17741002251547469f;
-
-// Box-Muller pair from words (wr, wa): R = sqrt(-2 ln u_r), angle 2 pi u_a.
-// u_r = 2 - f(wr) in (0,1]; the angle is evaluated as 2 pi (u_a - 1/2) in [-pi, pi) (MUFU's
-// accurate range) and the pair negated: (R cos 2pi u_a, R sin 2pi u_a) = -(R cos x, R sin x).
-__device__ __forceinline__ void box_muller(uint32_t wr, uint32_t wa, float& n0, float& n1) {
-  const float ur = 2.0f - word_to_f12(wr);
-  const float t = fmaxf(-1.38629436112f * lg2_approx(ur), 0.0f);   // -2 ln u_r
-  const float mr = -sqrt_approx(t);
-  const float x = (word_to_f12(wa) - 1.5f) * 6.28318530718f;
-  n0 = mr * cos_approx(x);
-  n1 = mr * sin_approx(x);
-}
 
 // The kernel's Box-Muller: returns (n0, n1) / BM_K.  sqrt(|log2 u_r|) replaces the clamp at 0 (log2 of
 // u_r <= 1 can come back ~1e-7 positive from MUFU.LG2); the angle 2 pi (u_a - 1/2) is one FFMA.
