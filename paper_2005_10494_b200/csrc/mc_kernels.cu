@@ -266,16 +266,16 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
           for (int i = 0; i < N; ++i) y[i] = sh.x[i] + sh.v[i];
 #pragma unroll
           for (int k = 0; k < KD; ++k) ind_count<N>(y, zc[k], cf[k]);
-          continue;
-        }
+        } else {
 #pragma unroll
-        for (int k = 0; k < KD; ++k) {
-          float b[N];
+          for (int k = 0; k < KD; ++k) {
+            float b[N];
 #pragma unroll
-          for (int i = 0; i < N; ++i) b[i] = zc[k][i] - sh.v[i];
-          float u = utility_of_b<N, EST, MODEL>(b, sh, pr);
-          if (MASKED) u = valid ? u : 0.0f;
-          accumulate<EST>(u, a1[k], a2[k]);
+            for (int i = 0; i < N; ++i) b[i] = zc[k][i] - sh.v[i];
+            float u = utility_of_b<N, EST, MODEL>(b, sh, pr);
+            if (MASKED) u = valid ? u : 0.0f;
+            accumulate<EST>(u, a1[k], a2[k]);
+          }
         }
       }
     }
