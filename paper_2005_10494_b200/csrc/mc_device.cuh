@@ -426,6 +426,171 @@ __device__ __forceinline__ float utility_of_b(const float* b, const Shared<N, ES
   return u;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Packed-pair COND path (sm_100a FFMA2/FMUL2/FADD2, `fma.rn.f32x2`).  A COND record holds R = 2
+// samples that run the identical instruction sequence on different data, so every FP32 operation of
+// the pair is ONE packed instruction: each lane is an IEEE fp32 op with round-to-nearest, exactly
+// what the scalar fmaf/mul/add computes, so the arithmetic per sample is unchanged (only ptxas's
+// contraction choices differ where the scalar path wrote a*b+c as two ops).  MUFU work (LG2, SQRT,
+// SIN, COS, RCP, EX2) and the selects stay scalar per lane.  The kernel is issue-bound,
+// so halving the FP32 instruction count is the lever.
+#ifndef MC_F32X2
+#define MC_F32X2 1
+#endif
+typedef unsigned long long f2x;   // (lo = sample 0, hi = sample 1)
+__device__ __forceinline__ f2x pk2(float lo, float hi) {
+  f2x r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi)); return r;
+}
+__device__ __forceinline__ f2x bc2(float c) { return pk2(c, c); }
+__device__ __forceinline__ void up2(f2x r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+  f2x d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+  f2x d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+  f2x d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d;
+}
+
+// normal_tail() for a pair: q = Phi(-a) and e = Phi(a) per lane, the same polynomial and the same
+// operation order (the exponent -a^2 + p(t) is formed as -(a a - p(t)) with the coefficients
+// negated, which is the same fp32 result; the minus sign rides on the EX2 operand).
+__device__ __forceinline__ void normal_tail2(f2x a, f2x& q, f2x& e) {
+  float a0, a1;
+  up2(a, a0, a1);
+  constexpr float K = (float)(0.28284271247461901 / 0.84932180028801904);
+  const f2x t = pk2(rcp_approx(fmaf(fabsf(a0), K, 1.0f)), rcp_approx(fmaf(fabsf(a1), K, 1.0f)));
+  f2x p = fma2(bc2(0.3020209548193252f), t, bc2(-1.3475361161107364f));
+  p = fma2(p, t, bc2(2.173205689641004f));
+  p = fma2(p, t, bc2(-1.4767906809187563f));
+  p = fma2(p, t, bc2(0.6654844086664139f));
+  p = fma2(p, t, bc2(-0.4449553247379003f));
+  p = fma2(p, t, bc2(-0.5735953408558541f));
+  p = fma2(p, t, bc2(-1.4456196577402736f));
+  p = fma2(p, t, bc2(3.1477861996521375f));        // -p(t)
+  const f2x s = fma2(a, a, p);                      // a^2 - p(t) = -(exponent)
+  float s0, s1;
+  up2(s, s0, s1);
+  const f2x ex = pk2(ex2_approx(-s0), ex2_approx(-s1));
+  const f2x qp = mul2(t, ex);                       // Phi(-|a|)
+  const f2x qc = fma2(qp, bc2(-1.0f), bc2(1.0f));   // Phi(|a|)
+  float qp0, qp1, qc0, qc1;
+  up2(qp, qp0, qp1);
+  up2(qc, qc0, qc1);
+  const bool pos0 = a0 >= 0.0f, pos1 = a1 >= 0.0f;
+  q = pk2(pos0 ? qp0 : qc0, pos1 ? qp1 : qc1);
+  e = pk2(pos0 ? qc0 : qp0, pos1 ? qc1 : qp1);
+}
+
+// normal_quantile_fast() for a pair (same polynomial, same clamp, reading R24).
+__device__ __forceinline__ f2x normal_quantile_fast2(f2x p, f2x pc) {
+  float m0, m1;
+  up2(mul2(p, pc), m0, m1);
+  f2x w2 = fma2(pk2(lg2_approx(m0), lg2_approx(m1)), bc2(-0.69314718056f), bc2(0.61370563888f));
+  float w0, w1;
+  up2(w2, w0, w1);
+  const f2x x = add2(pk2(sqrt_approx(fminf(w0, 18.0f)), sqrt_approx(fminf(w1, 18.0f))), bc2(-2.82842712474619f));
+  f2x g = fma2(bc2(-0.0001458914359425521f), x, bc2(0.00014054195626482066f));
+  g = fma2(g, x, bc2(0.0012376677239334937f));
+  g = fma2(g, x, bc2(-0.0017637622021570974f));
+  g = fma2(g, x, bc2(-0.0036462519812319317f));
+  g = fma2(g, x, bc2(0.009457966527136036f));
+  g = fma2(g, x, bc2(-0.0013609513949184736f));
+  g = fma2(g, x, bc2(-0.022852510105916587f));
+  g = fma2(g, x, bc2(0.04599717902636056f));
+  g = fma2(g, x, bc2(-0.040789581299890895f));
+  g = fma2(g, x, bc2(-0.018363709814932894f));
+  g = fma2(g, x, bc2(1.59782737417905f));
+  g = fma2(g, x, bc2(3.2334928032079135f));
+  return mul2(g, fma2(pc, bc2(-1.0f), p));          // g (p - pc)
+}
+
+// utility_of_b<N, 0, MODEL> for two lanes at once: thresholds b[i] and SOV uniforms vu[k] packed
+// (two samples of a record, or two designs sharing a sample under common random numbers).
+template <int N>
+__device__ __forceinline__ f2x utility_cond_x2(const f2x* b, const f2x* vu, const ProbRegs<N>& pr) {
+  constexpr int NE = N / 2, NO = (N + 1) / 2;
+  f2x uu = 0ull, q, e;
+  f2x x[NE > 0 ? NE : 1];
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+    const f2x a = k == 0 ? b[1] : fma2(bc2(-pr.er[k]), x[k > 0 ? k - 1 : 0], b[2 * k + 1]);
+    normal_tail2(a, q, e);
+    uu = k == 0 ? q : fma2(fma2(uu, bc2(-1.0f), bc2(1.0f)), q, uu);
+    const f2x v = vu[k];
+    const f2x vc = fma2(v, bc2(-1.0f), bc2(1.0f));                            // exact
+    const f2x y = normal_quantile_fast2(mul2(v, e), fma2(v, q, vc));
+    x[k] = k == 0 ? y : fma2(bc2(pr.esd[k]), y, mul2(bc2(pr.emu[k]), x[k > 0 ? k - 1 : 0]));
+  }
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    f2x a = b[2 * j];
+    if (2 * j >= 1) a = fma2(bc2(-pr.oa[j]), x[j > 0 ? j - 1 : 0], a);
+    if (2 * j + 1 < N) a = fma2(bc2(-pr.ob[j]), x[j < NE ? j : 0], a);
+    normal_tail2(a, q, e);
+    uu = (NE == 0 && j == 0) ? q : fma2(fma2(uu, bc2(-1.0f), bc2(1.0f)), q, uu);
+  }
+  return uu;
+}
+
+// Both utilities of a COND record (MODEL 0), packed: sample 0 in the low lane, sample 1 in the high lane.
+// Same words, same normals (pairs consumed in word order, cos first; sample h's normals at nrm + hP),
+// same stage order as utility_of_b<N, 0, 0>.
+template <int N>
+__device__ __forceinline__ void record_utility_cond_x2(const uint32_t* w, uint32_t one, const float* zc,
+                                                       const ProbRegs<N>& pr, float* u) {
+  using G = Geo<N, 0, 0>;
+  constexpr int P = G::P, NE = G::NE;
+  // Box-Muller (box_muller_scaled) with the radius and angle FFMAs of two word pairs packed
+  float mr[P], cs[P], sn[P];
+#pragma unroll
+  for (int j = 0; j < P; j += 2) {
+    float ur[2], xa[2];
+    if (j + 1 < P) {
+      up2(fma2(pk2(word_to_f12(w[2 * j], one), word_to_f12(w[2 * j + 2], one)), bc2(-1.0f), bc2(2.0f)),
+          ur[0], ur[1]);
+      up2(fma2(pk2(word_to_f12(w[2 * j + 1], one), word_to_f12(w[2 * j + 3], one)), bc2(6.28318530718f),
+               bc2(-9.42477796077f)), xa[0], xa[1]);
+    } else {
+      ur[0] = 2.0f - word_to_f12(w[2 * j], one);
+      xa[0] = fmaf(word_to_f12(w[2 * j + 1], one), 6.28318530718f, -9.42477796077f);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (j + h < P) {
+        mr[j + h] = -sqrt_approx(fabsf(lg2_approx(ur[h])));
+        cs[j + h] = cos_approx(xa[h]);
+        sn[j + h] = sin_approx(xa[h]);
+      }
+    }
+  }
+  // packed normals E[j] = (eps_j of sample 0, eps_j of sample 1) = (nrm[j], nrm[P + j])
+  f2x E[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int m0 = j, m1 = P + j;
+    E[j] = mul2(pk2(mr[m0 / 2], mr[m1 / 2]), pk2(m0 % 2 ? sn[m0 / 2] : cs[m0 / 2], m1 % 2 ? sn[m1 / 2] : cs[m1 / 2]));
+  }
+  // b = zc - M eps
+  f2x b[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    f2x acc = bc2(zc[i]);
+#pragma unroll
+    for (int j = 0; j <= i; ++j) acc = fma2(bc2(-pr.M[i * (i + 1) / 2 + j]), E[j], acc);
+    b[i] = acc;
+  }
+  f2x vu[NE > 0 ? NE : 1];
+#pragma unroll
+  for (int k = 0; k < NE; ++k)   // the SOV uniforms (k+1/2) 2^-23 of both samples
+    vu[k] = add2(pk2(word_to_f12(w[2 * P + k], one), word_to_f12(w[2 * P + NE + k], one)),
+                 bc2(-0.99999994039535522f));
+  up2(utility_cond_x2<N>(b, vu, pr), u[0], u[1]);
+}
+
 // Independent draws: the R utilities of one record, b formed directly from zc (FFMA chains seeded
 // with zc, no separate v).  If DBG, writes per sample the (unscaled) normals, b and u; bsc[i] (the
 // row scales) and BM_K undo the folding for the dump.
@@ -434,6 +599,26 @@ __device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, 
                                                const StrataRegs* sr, float* u, float* dbg = nullptr,
                                                const float* bsc = nullptr) {
   using G = Geo<N, EST, MODEL>;
+#if MC_F32X2
+  if constexpr (EST == 0 && MODEL == 0 && !DBG) {
+    record_utility_cond_x2<N>(w, one, zc, pr, u);
+    return;
+  }
+  if constexpr (EST == 0 && MODEL == 1 && !DBG) {   // C4 strata prior: b per sample, the SOV packed
+    float nrm[2 * G::NPAIR];
+    record_normals<N, EST, MODEL>(w, one, nrm);
+    Shared<N, EST, MODEL> sh0, sh1;
+    shared_of_sample<N, EST, MODEL>(nrm, w, 0, one, pr, sr, sh0);
+    shared_of_sample<N, EST, MODEL>(nrm, w, 1, one, pr, sr, sh1);
+    f2x b[N], vu[G::NE > 0 ? G::NE : 1];
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = pk2(zc[i] - sh0.v[i], zc[i] - sh1.v[i]);
+#pragma unroll
+    for (int k = 0; k < G::NE; ++k) vu[k] = pk2(sh0.vu[k], sh1.vu[k]);
+    up2(utility_cond_x2<N>(b, vu, pr), u[0], u[1]);
+    return;
+  }
+#endif
   float nrm[2 * G::NPAIR];
   record_normals<N, EST, MODEL>(w, one, nrm);
 #pragma unroll

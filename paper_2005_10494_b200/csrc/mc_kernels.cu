@@ -114,8 +114,20 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
         for (int r = 0; r < G::LR; ++r) {
           float u[G::R];
           record_utility<N, EST, false, MODEL>(&w[r * G::WR], one, zc, pr, &sr, u);
+#if MC_F32X2
+          if constexpr (EST == 0) {   // the pair's u + 1 and u u + 1 as one FADD2 and one FFMA2
+            const f2x uu = pk2(u[0], u[1]);
+            float s0, s1, t0, t1;
+            up2(add2(uu, bc2(1.0f)), s0, s1);
+            up2(fma2(uu, uu, bc2(1.0f)), t0, t1);
+            a1 += __float_as_uint(s0) + __float_as_uint(s1);
+            a2 += __float_as_uint(t0) + __float_as_uint(t1);
+          } else
+#endif
+          {
 #pragma unroll
-          for (int h = 0; h < G::R; ++h) accumulate_biased<EST>(u[h], a1, a2, cnt);
+            for (int h = 0; h < G::R; ++h) accumulate_biased<EST>(u[h], a1, a2, cnt);
+          }
         }
       }
       finish_biased<EST>(SAMPLES_PER_THREAD, a1, a2, cnt);
@@ -266,6 +278,27 @@ __device__ __forceinline__ void crn_samples(uint64_t s_begin, uint64_t B, uint64
           for (int i = 0; i < N; ++i) y[i] = sh.x[i] + sh.v[i];
 #pragma unroll
           for (int k = 0; k < KD; ++k) ind_count<N>(y, zc[k], cf[k]);
+        } else if constexpr (EST == 0 && MC_F32X2 && KD % 2 == 0) {
+          // COND: two designs of the block per packed lane pair (same sample, same SOV uniforms)
+          f2x nv[N], vu[G::NE > 0 ? G::NE : 1];
+#pragma unroll
+          for (int i = 0; i < N; ++i) nv[i] = bc2(-sh.v[i]);
+#pragma unroll
+          for (int k = 0; k < G::NE; ++k) vu[k] = bc2(sh.vu[k]);
+#pragma unroll
+          for (int k = 0; k < KD; k += 2) {
+            f2x b[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) b[i] = add2(pk2(zc[k][i], zc[k + 1][i]), nv[i]);
+            float u0, u1;
+            up2(utility_cond_x2<N>(b, vu, pr), u0, u1);
+            if (MASKED) {
+              u0 = valid ? u0 : 0.0f;
+              u1 = valid ? u1 : 0.0f;
+            }
+            accumulate<EST>(u0, a1[k], a2[k]);
+            accumulate<EST>(u1, a1[k + 1], a2[k + 1]);
+          }
         } else {
 #pragma unroll
           for (int k = 0; k < KD; ++k) {

@@ -115,6 +115,7 @@ def issue_per_draw(n: int = 3, est: int = 0, lib: str = None) -> float:
 
 
 FP32_OPS = ("FFMA", "FMUL", "FADD")       # the FP32 (FMA) pipe's arithmetic
+FP32X2_OPS = ("FFMA2", "FMUL2", "FADD2")  # packed pairs: one issue slot, two FP32 lane-ops
 SFU_OPS = ("MUFU",)
 
 
@@ -126,7 +127,7 @@ def pipe_mix(n: int = 3, est: int = 0, lib: str = None) -> dict:
     ops = [(t.split()[1] if t.startswith("@") else t.split()[0]) for _, t in path]
     base = [o.split(".")[0] for o in ops]
     return {"issue": len(path) / L,
-            "fp32": sum(b in FP32_OPS for b in base) / L,
+            "fp32": (sum(b in FP32_OPS for b in base) + 2 * sum(b in FP32X2_OPS for b in base)) / L,
             "sfu": sum(b in SFU_OPS for b in base) / L,
             "imad_wide": sum(o.startswith("IMAD.WIDE") for o in ops) / L}
 
