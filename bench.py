@@ -33,8 +33,8 @@ from paper_2005_10494_b200 import workloads as W  # noqa: E402
 # Per-draw issue slots of the fused kernel's steady-state loop (n = 3), counted from the sm_100a SASS
 # of the library being timed by tools/sass_count.py: the ALU/issue roofline's work per
 # draw.  The fallback constants are that tool's output for the committed kernel.
-ISSUE_PER_DRAW_FALLBACK = {"cond": 145.5, "ind": 108.0}
-PIPE_MIX_FALLBACK = {"cond": {"issue": 145.5, "fp32": 78.5, "sfu": 14.0, "imad_wide": 18.0},
+ISSUE_PER_DRAW_FALLBACK = {"cond": 112.5, "ind": 108.0}
+PIPE_MIX_FALLBACK = {"cond": {"issue": 112.5, "fp32": 78.5, "sfu": 14.0, "imad_wide": 18.0},
                      "ind": {"issue": 108.0, "fp32": 26.0, "sfu": 12.0, "imad_wide": 27.0}}
 
 
@@ -301,8 +301,8 @@ def run_ours(args):
                 "frac": round(mix["sfu"] * rate / (16 * sm_count * fmax), 4)}}
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "Tinst/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "traffic_ncu": {"dram_bytes_per_launch": 448256, "draws_per_launch": 1.2e10,
-                            "capture": "profiles/r01/ncu_fused_cond_summary.txt (--problems 6; the full C2 launch "
+            "traffic_ncu": {"dram_bytes_per_launch": 507904, "draws_per_launch": 1.2e10,
+                            "capture": "profiles/r01/ncu_fused_cond_x2_summary.txt (--problems 6; the full C2 launch "
                                        "times out under --set full replay)",
                             "note": "DRAM bytes scale with designs (zc, problem_of_design, sums), not draws: "
                                     "~4e-5 B/draw; the kernel does no HBM work per draw"},
