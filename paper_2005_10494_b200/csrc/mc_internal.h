@@ -25,13 +25,13 @@ constexpr int OFF_STR = 112;             // C4 strata model: 17 floats (mc_devic
 constexpr int SAMPLES_PER_THREAD = 128;  // per-thread sample run inside a warp tile (< 512: u32 sums)
 constexpr int MAX_BLOCK = 256;           // fused kernel __launch_bounds__
 #ifndef MC_MIN_BLOCKS_COND
-#define MC_MIN_BLOCKS_COND 4
+#define MC_MIN_BLOCKS_COND 5
 #endif
 #ifndef MC_MIN_BLOCKS_IND
 #define MC_MIN_BLOCKS_IND 5
 #endif
-constexpr int MIN_BLOCKS_COND = MC_MIN_BLOCKS_COND;   // min resident 256-thread blocks per SM, n <= 3
-constexpr int MIN_BLOCKS_IND = MC_MIN_BLOCKS_IND;     //   (register caps 64 / 48)
+constexpr int MIN_BLOCKS_COND = MC_MIN_BLOCKS_COND;   // min resident 256-thread blocks per SM, n <= 3 (COND 5: +1.9 % with the packed pair, profiles/r01/tune_f32x2.jsonl)
+constexpr int MIN_BLOCKS_IND = MC_MIN_BLOCKS_IND;     //   (register caps 48 / 48)
 
 void set_error(const std::string& msg);
 mc_status cuda_fail(cudaError_t e, const char* where);

@@ -86,7 +86,11 @@ __device__ __forceinline__ void finish_biased(uint32_t draws, uint32_t& a1, uint
 #ifndef MC_STEP_UNROLL
 #define MC_STEP_UNROLL 1
 #endif
+#ifndef MC_STEP_UNROLL_COND
+#define MC_STEP_UNROLL_COND MC_STEP_UNROLL
+#endif
 constexpr int kStepUnroll = MC_STEP_UNROLL;   // steady-loop unroll (pragma arguments are not macro-expanded)
+constexpr int kStepUnrollCond = MC_STEP_UNROLL_COND;
 template <int N, int EST, bool MASKED, int MODEL>
 __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64_t E, uint32_t lo1d, uint32_t hi1d,
                                             const RoundKeys& rk, const float* zc, const ProbRegs<N>& pr,
@@ -104,7 +108,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
       const uint32_t c0r1 = hi1d ^ (uint32_t)(q >> 32) ^ rk.k0[0];
       uint32_t ql = q0;
       float cnt = 0.0f;
-#pragma unroll kStepUnroll
+#pragma unroll(EST == 0 ? kStepUnrollCond : kStepUnroll)
       for (int st = 0; st < STEPS; ++st) {
         uint32_t w[G::BLOCKS * 4];
 #pragma unroll
