@@ -220,10 +220,10 @@ __global__ void __launch_bounds__(MAX_BLOCK, min_blocks(N, EST, MODEL)) mc_fused
 // (q_lo, q_hi, problem, 1)); every design of the problem sees the same draws, so the design-
 // independent part of a draw (Philox, Box-Muller, the prior term, the IND null vector, the SOV
 // uniforms) is computed once and reused for a block of CRN_KD designs held in registers.
-// designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 12 / 1 (3.34e11/s; 4 / 2 gave 2.98e11),
+// designs per CRN warp tile and min resident blocks (measured on B200, tools/tune_crn.sh): COND 16 / 1 (packed FP32 design pairs: 3.65e11/s vs 3.60e11 with 12, 3.45e11 with 8; scalar 12: 3.34e11),
 // IND 32 / 1 (IND: one shared y = X + v per sample, 3 compares + 1 predicated FADD per design: 2.74e12/s)
 #ifndef MC_CRN_KD_COND
-#define MC_CRN_KD_COND 12
+#define MC_CRN_KD_COND 16
 #endif
 #ifndef MC_CRN_KD_IND
 #define MC_CRN_KD_IND 32
