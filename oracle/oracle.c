@@ -364,40 +364,36 @@ void or_design_sums(int n, int p, const double *r, double i3, const double *thet
 }
 
 /* ------------------------------------------------------------------------- */
-/* Gauss-Legendre rule on [-1,1] by Newton iteration on P_G (textbook).       */
-static void gauss_legendre(int G, double *x, double *w)
+/* Gauss-Legendre rule on [-1,1]: nodes and weights are SUPPLIED by the caller
+ * (oracle.py passes numpy.polynomial.legendre.leggauss(20), a library routine),
+ * so this file computes no quadrature rule of its own.                       */
+enum { OR_GL_MAX = 64 };
+static int or_gl_n = 0;
+static double or_gl_x[OR_GL_MAX], or_gl_w[OR_GL_MAX];
+
+int or_set_gauss_legendre(int G, const double *x, const double *w)
 {
-    for (int i = 0; i < G; ++i) {
-        double t = cos(M_PI * (i + 0.75) / (G + 0.5)), dp = 0.0;
-        for (int it = 0; it < 100; ++it) {
-            double p0 = 1.0, p1 = t;
-            for (int k = 2; k <= G; ++k) { double p2 = ((2.0 * k - 1.0) * t * p1 - (k - 1.0) * p0) / k; p0 = p1; p1 = p2; }
-            dp = G * (t * p1 - p0) / (t * t - 1.0);
-            double dt = p1 / dp;
-            t -= dt;
-            if (fabs(dt) < 1e-16) break;
-        }
-        x[i] = t;
-        w[i] = 2.0 / ((1.0 - t * t) * dp * dp);
-    }
+    if (G < 2 || G > OR_GL_MAX) return 1;
+    for (int i = 0; i < G; ++i) { or_gl_x[i] = x[i]; or_gl_w[i] = w[i]; }
+    or_gl_n = G;
+    return 0;
 }
 
-/* Composite Gauss-Legendre nodes on [a, b] with panels no wider than h. */
+/* Composite Gauss-Legendre nodes on [a, b] with panels no wider than h.
+ * Returns the node count, or -1 if the nodes would not fit in cap.           */
 static int panel_nodes(double a, double b, double h, double *xs, double *ws, int cap)
 {
-    enum { G = 10 };
-    double gx[G], gw[G];
-    gauss_legendre(G, gx, gw);
+    const int G = or_gl_n;
     if (!(b > a)) return 0;
     int P = (int)ceil((b - a) / h);
-    if (P * G > cap) P = cap / G;
+    if ((long)P * G > cap) return -1;
     double len = (b - a) / P;
     int m = 0;
     for (int k = 0; k < P; ++k) {
         double lo = a + k * len;
         for (int g = 0; g < G; ++g) {
-            xs[m] = lo + 0.5 * len * (gx[g] + 1.0);
-            ws[m] = 0.5 * len * gw[g];
+            xs[m] = lo + 0.5 * len * (or_gl_x[g] + 1.0);
+            ws[m] = 0.5 * len * or_gl_w[g];
             ++m;
         }
     }
@@ -413,25 +409,36 @@ static double phi_pdf(double x) { return exp(-0.5 * x * x) / sqrt(2.0 * M_PI); }
  *   Phi = int_{-inf}^{b_1} phi(x_1) h_1(x_1) dx_1,
  *   h_k(x) = int_{-inf}^{b_{k+1}} phi((y - rho_k x)/s_k)/s_k h_{k+1}(y) dy,
  *   h_{n-1}(x) = Phi((b_n - rho_{n-1} x)/s_{n-1}),
- * evaluated with composite Gauss-Legendre on [-9, min(b_k, 9)] (mass outside < 1e-18). */
+ * evaluated with composite Gauss-Legendre (the supplied G-point rule) on [-10, min(b_k, 10)]
+ * (mass outside < 1e-23) with panels no wider than the narrowest conditional sd s_j.
+ * Returns NAN if no rule was supplied or a level would need more than CAP nodes.
+ * (Level storage is allocated per call: the oracle is single-threaded per process.)      */
 double or_mvn_orthant(int n, const double *r, const double *b)
 {
     if (n == 1) return or_Phi(b[0]);
+    if (or_gl_n == 0) return NAN;
     double rho[OR_MAXN], sd[OR_MAXN], smin = 1.0;
     for (int k = 0; k + 1 < n; ++k) {
         rho[k] = sqrt(r[k + 1] / r[k]);
         sd[k] = sqrt(1.0 - r[k + 1] / r[k]);
         if (sd[k] < smin) smin = sd[k];
     }
-    const double LO = -9.0, HI = 9.0;
-    double h = 0.5 * smin; if (h > 0.5) h = 0.5;
-    enum { CAP = 8000 };
-    static double xs[OR_MAXN][CAP], ws[OR_MAXN][CAP], hv[OR_MAXN][CAP];
+    const double LO = -10.0, HI = 10.0;
+    double h = smin;
+    enum { CAP = 1000000 };
+    const int need = or_gl_n * (int)ceil((HI - LO) / h);
+    if (need > CAP) return NAN;
+    double *xs[OR_MAXN], *ws[OR_MAXN], *hv[OR_MAXN];
+    double *buf = (double *)malloc(sizeof(double) * 3 * (size_t)need * (n - 1));
+    if (!buf) return NAN;
     int m[OR_MAXN];
     for (int k = 0; k + 1 < n; ++k) {
+        xs[k] = buf + (size_t)need * (3 * k);
+        ws[k] = xs[k] + need;
+        hv[k] = ws[k] + need;
         double up = b[k] < HI ? b[k] : HI;
-        if (up <= LO) return 0.0;
-        m[k] = panel_nodes(LO, up, h, xs[k], ws[k], CAP);
+        if (up <= LO) { free(buf); return 0.0; }
+        m[k] = panel_nodes(LO, up, h, xs[k], ws[k], need);
     }
     /* level n-1 (0-based n-2): closed-form last conditional */
     int L = n - 2;
@@ -447,6 +454,7 @@ double or_mvn_orthant(int n, const double *r, const double *b)
     }
     double acc = 0.0;
     for (int j = 0; j < m[0]; ++j) acc += ws[0][j] * phi_pdf(xs[0][j]) * hv[0][j];
+    free(buf);
     return acc;
 }
 
@@ -460,7 +468,8 @@ double or_fwer(int n, const double *r, const double *alpha)
 
 /* Sec. 2.1 re-parametrisation: solve FWER(alpha_1..alpha_{n-1}, a) = alpha0 for
  * a in [0, alpha0] by bisection (FWER is increasing in a).  Returns 1 and writes *an
- * when feasible; 0 when FWER(.., 0) > alpha0 (reading R12: the point is invalid). */
+ * when feasible; 0 when FWER(.., 0) > alpha0 (reading R12: the point is invalid);
+ * -1 when the orthant quadrature is unavailable (or_mvn_orthant returned NAN).          */
 int or_solve_alpha_n(int n, const double *r, double alpha0, const double *partial, double tol, double *an)
 {
     double a[OR_MAXN];
@@ -469,6 +478,7 @@ int or_solve_alpha_n(int n, const double *r, double alpha0, const double *partia
     a[n - 1] = 0.0;
     /* FWER(.., 0) decides feasibility up to quadrature rounding: |err| < 1e-12 (R12). */
     double f0 = or_fwer(n, r, a) - alpha0;
+    if (isnan(f0)) return -1;                      /* quadrature unavailable / under-resolved */
     if (f0 > 1e-12) return 0;
     if (f0 >= -1e-12) { *an = 0.0; return 1; }
     double lo = 0.0, hi = alpha0;
@@ -483,7 +493,8 @@ int or_solve_alpha_n(int n, const double *r, double alpha0, const double *partia
 
 /* Sec. 2.3: the m^(n-1) half-offset grid alpha_j = (k_j + 1/2) alpha0 / m on
  * (0, alpha0)^(n-1) (reading R8/R10), first coordinate slowest.  Writes every grid
- * point's feasibility flag and solved alpha_n.  Returns the number of grid points.   */
+ * point's feasibility flag and solved alpha_n.  Returns the number of grid points, or -1
+ * if the orthant quadrature is unavailable for r.                                      */
 int64_t or_alpha_grid(int n, const double *r, double alpha0, int m, double tol,
                       double *alpha_out /* [m^(n-1) * n] */, uint8_t *valid_out)
 {
@@ -495,6 +506,7 @@ int64_t or_alpha_grid(int n, const double *r, double alpha0, int m, double tol,
         for (int i = n - 2; i >= 0; --i) { part[i] = ((double)(rem % m) + 0.5) * alpha0 / m; rem /= m; }
         double an = 0.0;
         int ok = or_solve_alpha_n(n, r, alpha0, part, tol, &an);
+        if (ok < 0) return -1;                         /* quadrature unavailable */
         for (int i = 0; i + 1 < n; ++i) alpha_out[g * n + i] = part[i];
         alpha_out[g * n + n - 1] = ok ? an : NAN;
         valid_out[g] = (uint8_t)ok;

@@ -25,6 +25,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 MAXN = 10
+GL_NODES = 20   # Gauss-Legendre points per panel of the MVN orthant quadrature (numpy leggauss)
 
 
 def build(force: bool = False) -> str:
@@ -69,6 +70,12 @@ def lib():
         L.or_draw_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u32, u64, P(d), P(d), P(d), P(d)]
         L.or_draw_strata.restype = d
         L.or_design_sums_strata.argtypes = [d, d, P(d), P(d), i32, u64, u32, u32, u64, u64, P(i64)]
+        L.or_set_gauss_legendre.argtypes = [i32, P(d), P(d)]; L.or_set_gauss_legendre.restype = i32
+        # the orthant quadrature's rule: numpy's 20-point Gauss-Legendre nodes and weights (a library
+        # routine; oracle.c computes none of its own)
+        gx, gw = np.polynomial.legendre.leggauss(GL_NODES)
+        if L.or_set_gauss_legendre(GL_NODES, _dp(gx), _dp(gw)) != 0:
+            raise RuntimeError("or_set_gauss_legendre rejected the rule")
         _lib = L
     return _lib
 
@@ -90,6 +97,11 @@ def philox4x32_10(ctr, key):
 
 def word(seed: int, design: int, w: int) -> int:
     return int(lib().or_word(seed, design, w))
+
+
+def word_tagged(seed: int, ident: int, tag: int, w: int) -> int:
+    """Word w of stream (id, tag): lane w mod 4 of the block with counter (q_lo, q_hi, id, tag)."""
+    return int(lib().or_word_tagged(seed, ident, tag, w))
 
 
 def words_per_draw(n: int, p: int, est: int) -> int:
@@ -253,6 +265,8 @@ def solve_alpha_n(r, alpha0: float, partial, tol: float = 1e-13):
     out = ctypes.c_double(0.0)
     ok = lib().or_solve_alpha_n(len(r), _dp(r), float(alpha0), _dp(np.asarray(partial, dtype=np.float64)),
                                 tol, ctypes.byref(out))
+    if ok < 0:
+        raise ValueError("solve_alpha_n: the orthant quadrature is unavailable for this r (node cap)")
     return float(out.value) if ok else None
 
 
@@ -285,8 +299,9 @@ def alpha_grid(r, alpha0: float, m: int, tol: float = 1e-13):
     G = m ** (n - 1)
     A = np.zeros((G, n))
     V = np.zeros(G, dtype=np.uint8)
-    lib().or_alpha_grid(n, _dp(r), float(alpha0), int(m), tol, A.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-                        V.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+    if lib().or_alpha_grid(n, _dp(r), float(alpha0), int(m), tol, A.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                           V.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))) < 0:
+        raise ValueError("alpha_grid: the orthant quadrature is unavailable for this r (node cap)")
     return A, V.astype(bool)
 
 

@@ -111,3 +111,16 @@ def test_fwer_examples_and_monotone(O):
         a = list(base)
         a[i] += 1e-4
         assert O.fwer(r, a) > f0
+
+
+def test_orthant_n4_close_ratios_vs_genz(O):
+    """n = 4 with adjacent r ratios 0.99 (conditional sd 0.1): against scipy's Genz integration and the
+    FWER bounds max(alpha) <= FWER <= sum(alpha) (the quadrature must follow the narrowest sd)."""
+    r = [1.0, 0.99, 0.98, 0.97]
+    S = O.null_corr(r)
+    b = np.array([2.2, 2.0, 2.5, 1.9])
+    ref = stats.multivariate_normal(mean=np.zeros(4), cov=S, abseps=1e-9, releps=1e-9, maxpts=20_000_000).cdf(b)
+    assert O.mvn_orthant(r, b) == pytest.approx(ref, abs=2e-6)
+    a = np.array([0.006, 0.006, 0.006, 0.006])
+    f = O.fwer(r, a)
+    assert a.max() < f < a.sum()
