@@ -152,7 +152,9 @@ void mc_destroy(mc_ctx* ctx);
  * (design, sample)-keyed Philox stream, evaluates the per-draw utility u and ACCUMULATES the exact
  * integer sums (sum round(2^23 u), sum round(2^23 u^2)) into sums_dev[D*2] (int64, caller zeroes;
  * entry 2d, 2d+1 for design d).  Integer accumulation makes the result bit-identical for every
- * split of the samples over calls, launch shapes and GPUs.  Asynchronous. */
+ * split of the samples over calls, launch shapes and GPUs.  sample_begin +
+ * sample_count must be < 2^40 (MC_ERR_INVALID otherwise), and the samples accumulated into one sums
+ * buffer must total < 2^40 per design: S1, S2 <= samples x 2^23 must stay below 2^63.  Asynchronous. */
 mc_status mc_evaluate_grid(mc_ctx* ctx, int64_t design_begin, int64_t design_count,
                            uint64_t sample_begin, uint64_t sample_count, void* cuda_stream,
                            int64_t* sums_dev);
@@ -162,7 +164,7 @@ mc_status mc_evaluate_grid(mc_ctx* ctx, int64_t design_begin, int64_t design_cou
  * with N2 inner null draws x^(l) (stream (d, tag 3), 2ceil(n/2) words per draw) — all N1 N2 pairs.
  * ACCUMULATES the exact integers S1 = sum_k c_k and S2 = sum_k c_k^2 into sums_dev[D*2], with
  * c_k = #{l : exists i x_i^(l) > b_i^(k)}.  The ctx must be built with MC_EST_IND and a Gaussian prior;
- * n <= 4; N2 < 2^32.  Asynchronous. */
+ * n <= 4; N2 < 2^32 and N1 N2^2 < 2^63 (S2 is an int64; MC_ERR_INVALID otherwise).  Asynchronous. */
 mc_status mc_evaluate_crossed(mc_ctx* ctx, uint64_t n1, uint64_t n2, void* cuda_stream, int64_t* sums_dev);
 
 /* Crossed finalize: mean_d = S1/(N1 N2); var_d = sample variance over k of c_k/N2 (the outer-draw
@@ -259,13 +261,19 @@ int32_t mc_num_problems(const mc_ctx* ctx);
  * each sample's floor(n/2) SOV uniforms.  -1 for a null ctx. */
 int32_t mc_words_per_draw(const mc_ctx* ctx);
 
-/* K3: Philox words.  out_dev[i] = word word_dev[i] of design design_dev[i]'s stream for `seed`
- * (DESIGN.md §2.2).  count entries.  Asynchronous. */
-mc_status mc_philox_dump(uint64_t seed, const uint32_t* design_dev, const uint64_t* word_dev,
+/* K3 (test hook): Philox words exactly as the kernels generate them.  out_dev[i] = word word_dev[i] of
+ * the stream (id_dev[i], tag) for `seed` (lane w mod 4 of the block with counter
+ * (q_lo, q_hi, id, tag), q = w / 4).  tag: 0 independent draws (id = design), 1 common random numbers
+ * (id = problem), 2 / 3 the crossed estimator's outer / inner streams.  form: 0 the fused and CRN kernels'
+ * steady-state block (round 1 hoisted, constant-bank round keys), 1 the fused kernel's masked-path block
+ * (tag 0 only), 2 the plain ten-round block of the crossed kernel.  count entries; MC_ERR_INVALID for a
+ * bad form.  Asynchronous. */
+mc_status mc_philox_dump(uint64_t seed, uint32_t tag, int32_t form, const uint32_t* id_dev, const uint64_t* word_dev,
                          int64_t count, uint32_t* out_dev, void* cuda_stream);
 
 /* Per-draw record of (design_dev[i], sample_dev[i]) computed by the same device code as the fused
- * kernel: out_dev[i*stride ...] = normals (p prior, then n null for IND), b[n], u; stride = p + 2n + 1
+ * kernel (the steady-state Philox form; COND: the packed two-sample record code of K1):
+ * out_dev[i*stride ...] = normals (p prior, then n null for IND), b[n], u; stride = p + 2n + 1
  * (IND) or p + n + 1 (COND), fp32.  Asynchronous. */
 mc_status mc_draw_dump(mc_ctx* ctx, const int64_t* design_dev, const uint64_t* sample_dev,
                        int64_t count, float* out_dev, void* cuda_stream);

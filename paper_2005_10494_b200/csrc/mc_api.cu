@@ -458,7 +458,10 @@ mc_status mc_evaluate_grid(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t s0, u
   if (!c || !sums) { set_error("mc_evaluate_grid: null ctx or sums"); return MC_ERR_INVALID; }
   if (d0 < 0 || dcount < 0 || d0 + dcount > c->D) { set_error("mc_evaluate_grid: design range outside [0, D)"); return MC_ERR_INVALID; }
   if (scount > 0 && s0 + scount < s0) { set_error("mc_evaluate_grid: sample range overflows"); return MC_ERR_INVALID; }
-  if ((s0 + scount) > ((uint64_t)1 << 40)) { set_error("mc_evaluate_grid: samples beyond 2^40 per design overflow the int64 sums"); return MC_ERR_INVALID; }
+  // S1, S2 <= (samples accumulated) x 2^23 must stay below 2^63: the sample indices stay below 2^40
+  // (exactly 2^40 samples of u = 1 would reach 2^63).  The bound covers one call; sums accumulated over
+  // several calls into the same buffer must also total fewer than 2^40 samples per design (header).
+  if ((s0 + scount) >= ((uint64_t)1 << 40)) { set_error("mc_evaluate_grid: sample indices must stay below 2^40 (int64 sums overflow at 2^40 x 2^23)"); return MC_ERR_INVALID; }
   MC_CUDA(cudaSetDevice(c->device));
   return launch_fused(c, d0, dcount, s0, s0 + scount, (cudaStream_t)stream, sums);
 }
@@ -500,10 +503,10 @@ int32_t mc_words_per_draw(const mc_ctx* c) { return c ? words_per_draw(c->n, c->
 int32_t mc_draw_dump_stride(const mc_ctx* c) { return c ? draw_dump_stride(c->n, c->est, c->model) : -1; }
 int64_t mc_kernel_launches(const mc_ctx* c) { return c ? c->launches.load() : (int64_t)-1; }
 
-mc_status mc_philox_dump(uint64_t seed, const uint32_t* design, const uint64_t* word, int64_t count, uint32_t* out,
-                         void* stream) {
-  if (count > 0 && (!design || !word || !out)) { set_error("mc_philox_dump: null pointer"); return MC_ERR_INVALID; }
-  return launch_philox_dump(seed, design, word, count, out, (cudaStream_t)stream);
+mc_status mc_philox_dump(uint64_t seed, uint32_t tag, int32_t form, const uint32_t* id, const uint64_t* word,
+                         int64_t count, uint32_t* out, void* stream) {
+  if (count > 0 && (!id || !word || !out)) { set_error("mc_philox_dump: null pointer"); return MC_ERR_INVALID; }
+  return launch_philox_dump(seed, tag, form, id, word, count, out, (cudaStream_t)stream);
 }
 
 mc_status mc_draw_dump(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,

@@ -164,6 +164,11 @@ mc_status mc_evaluate_crossed(mc_ctx* c, uint64_t n1, uint64_t n2, void* stream,
     set_error("mc_evaluate_crossed: N2 must be < 2^32");
     return MC_ERR_INVALID;
   }
+  // S2 = sum_k c_k^2 <= N1 N2^2 must fit the int64 that k_finalize_crossed reads
+  if ((unsigned __int128)n1 * n2 * n2 >= ((unsigned __int128)1 << 63)) {
+    set_error("mc_evaluate_crossed: N1 N2^2 must be < 2^63 (the int64 sum of c_k^2 would overflow)");
+    return MC_ERR_INVALID;
+  }
   MC_CUDA(cudaSetDevice(c->device));
   const int64_t obpd = (int64_t)((n1 + XO_THREADS * XO_KO - 1) / (XO_THREADS * XO_KO));
   const int64_t blocks = obpd * c->D;

@@ -37,7 +37,6 @@ struct Geo {
 
 // ---------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11).  Counter (q_lo, q_hi, design, 0), key (seed_lo, seed_hi).
-struct Key { uint32_t k0, k1; };
 // The ten round keys (k0 + r W0, k1 + r W1), r = 0..9, precomputed on the host and passed by value
 // as a kernel parameter: the rounds then read them straight from the constant bank (no key schedule
 // in the loop).
@@ -74,28 +73,6 @@ __device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_
   c3 = lo0;
 }
 
-// One block for counter (q, design, 0).  The first round's c2-product depends only on the
-// design, so callers pass it precomputed (lo1d = M1*design, hi1d = umulhi(M1, design)).
-__device__ __forceinline__ void philox_block(uint64_t q, uint32_t lo1d, uint32_t hi1d, Key key,
-                                             uint32_t out[4]) {
-  const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32);
-  // round 1 with c2 = design, c3 = 0
-  uint32_t hq, lq;
-  mulhilo(q0, 0xD2511F53u, hq, lq);
-  uint32_t c0 = hi1d ^ q1 ^ key.k0;
-  uint32_t c1 = lo1d;
-  uint32_t c2 = hq ^ key.k1;
-  uint32_t c3 = lq;
-  uint32_t k0 = key.k0, k1 = key.k1;
-#pragma unroll
-  for (int r = 1; r < 10; ++r) {
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-    philox_round(c0, c1, c2, c3, k0, k1);
-  }
-  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
-}
-
 // Same block with the precomputed round keys (the fused kernel's form).
 __device__ __forceinline__ void philox_block_rk(uint64_t q, uint32_t lo1d, uint32_t hi1d, const RoundKeys& rk,
                                                 uint32_t out[4]) {
@@ -126,13 +103,6 @@ __device__ __forceinline__ void philox_block_lo(uint32_t q0, uint32_t c0r1, uint
 #pragma unroll
   for (int r = 1; r < 10; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
   out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
-}
-
-__device__ __forceinline__ uint32_t philox_word(uint64_t seed, uint32_t design, uint64_t w) {
-  Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
-  uint32_t o[4];
-  philox_block(w >> 2, 0xCD9E8D57u * design, __umulhi(0xCD9E8D57u, design), key, o);
-  return o[w & 3];
 }
 
 // Word w of the stream (id, tag): counter (q_lo, q_hi, id, tag) — plain 10-round form (test hooks).
@@ -185,60 +155,55 @@ __device__ __forceinline__ void box_muller_scaled(uint32_t wr, uint32_t wa, uint
   n1 = mr * sin_approx(x);
 }
 
-// Upper normal tail q = Phi(-a) for a >= 0 in the Numerical-Recipes erfc form (Press et al., "erfcc":
-// t = 1/(1 + kappa a), q = t exp(-a^2/2 + poly(t))) refitted in base 2 with a degree-8 polynomial
-// (tools/fit_normal_tail.py: kappa = 0.4/sqrt2, max relative error 9.2e-8 in exact arithmetic): one RCP,
-// eight FFMAs, one EX2 on the MUFU pipe.  Returns q and e = 1 - q (= Phi(a)) without cancellation for
-// either sign of a.  The argument arrives PRE-SCALED, a' = a sqrt(log2(e)/2) (the COND record folds the
-// factor into M, the thresholds and the stage coefficients: mc_api.cu PHI_SCALE), so the exponent
-// -a^2 log2(e)/2 = -a'^2 is one FFMA and kappa becomes kappa / sqrt(log2(e)/2).
+// Upper normal tail q = Phi(-x), x >= 0, as ONE power of two: q = 2^E(m), m = min(|a|, PHI_CLAMP), E a
+// degree-11 polynomial in m that includes the -a^2 term (tools/fit_normal_tail_ex2.py: relative error
+// 3.6e-8 in exact arithmetic, 1.4e-6 in fp32 for x <= 4).  The argument arrives PRE-SCALED,
+// a = x sqrt(log2(e)/2) (the COND record folds the factor into M, the thresholds and the stage
+// coefficients: mc_api.cu PHI_SCALE), so E ~ -a^2.  Beyond the clamp (x > 5.887) q is held at
+// q(5.887) = 2.0e-9, a change below 2^-28 that the per-draw 2^-23 fixed point absorbs; alpha = 0
+// (z = +inf, a = +inf) therefore gives u = 0 exactly.  One MUFU (EX2), no reciprocal: round 1's
+// Numerical-Recipes form t = 1/(1 + kappa x), q = t 2^(P(t) - a^2) needed RCP + EX2 per call.
+// Returns q and e = 1 - q (= Phi(x)) without cancellation for either sign of a.
+constexpr float PHI_CLAMP = 5.0f;
+#define MC_PHI_POLY(HORNER, m)                                       \
+  HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER( \
+      1.3214344735792895e-08f, m, -4.290973434515816e-07f), m, 6.177874180542052e-06f), m,                   \
+      -5.145014405324849e-05f), m, 0.0002655422273086682f), m, -0.0007692117070775829f), m,                    \
+      -1.9095885481130195e-05f), m, 0.013417788461371934f), m, -0.08565676580912412f), m,                      \
+      -0.6365931830340086f), m, -1.355324411309415f), m, -0.9999999477305315f)
+__device__ __forceinline__ float horner1(float p, float x, float c) { return fmaf(p, x, c); }
+
 __device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
-  const float aa = fabsf(a);
-  const float t = rcp_approx(fmaf(aa, (float)(0.28284271247461901 / 0.84932180028801904), 1.0f));
-  float p = -0.3020209548193252f;
-  p = fmaf(p, t, 1.3475361161107364f);
-  p = fmaf(p, t, -2.173205689641004f);
-  p = fmaf(p, t, 1.4767906809187563f);
-  p = fmaf(p, t, -0.6654844086664139f);
-  p = fmaf(p, t, 0.4449553247379003f);
-  p = fmaf(p, t, 0.5735953408558541f);
-  p = fmaf(p, t, 1.4456196577402736f);
-  p = fmaf(p, t, -3.1477861996521375f);
-  const float ex = ex2_approx(fmaf(-aa, aa, p));   // -a'^2 = -a^2 log2(e) / 2
-  const float qp = t * ex;                     // Phi(-|a|)
-  const float qc = 1.0f - qp;                  // Phi(|a|)
+  const float m = fminf(fabsf(a), PHI_CLAMP);
+  const float qp = ex2_approx(MC_PHI_POLY(horner1, m));   // Phi(-|x|)
+  const float qc = 1.0f - qp;                              // Phi(|x|)
   const bool pos = a >= 0.0f;
   q = pos ? qp : qc;
   e = pos ? qc : qp;
 }
 
 // Standard normal quantile Phi^{-1}(p) given p and its complement pc = 1 - p (both computed accurately by
-// the caller), via erfinv(y) = g(w) y, y = 2p - 1 = p - pc, w = -ln(4 p pc), for w in [0, 16]
-// (p in [2.8e-8, 1 - 2.8e-8]): ONE degree-12 polynomial in sqrt(w + 2) (tools/fit_erfinv_single.py,
-// relative error 5.3e-7 in fp32; sqrt(2) folded into the coefficients) — no per-coefficient selects on
-// the ALU pipe and no branch.  Beyond that range the argument is clamped to w = 16 (reading R24): in the
-// SOV this only happens when v e_k < 2.8e-8 (the upper side cannot clamp: 1 - v >= 2^-24), and the
-// resulting change of u is at most e_k on an event of probability <= 2.8e-8 / e_k, i.e. a bias of at
-// most 2.8e-8 per even stage.  Replacing the deep-tail branch (BSSY/FSETP/BRA/BSYNC per call and warp
-// divergence) measured +4.8 % draws/s on C2 (profiles/r01/tune_grid.txt).
+// the caller): Phi^{-1}(p) = g(t) (p - pc) with t = w/8 - 1, w = -ln(4 p pc) in [0, 16]
+// (p in [2.8e-8, 1 - 2.8e-8]), g ONE degree-14 polynomial in t (tools/fit_erfinv_w.py: relative error
+// 6.0e-8 in exact arithmetic, 9.6e-7 in fp32) — no square root, no per-coefficient selects and no branch.
+// t = lg2(p pc) (-ln2/8) + (-ln4/8 - 1) is one FFMA after MUFU.LG2.  Beyond that range t is clamped to 1
+// (w = 16, reading R24): in the SOV this only happens when v e_k < 2.8e-8 (the upper side cannot clamp:
+// 1 - v >= 2^-24), and the resulting change of u is at most e_k on an event of probability
+// <= 2.8e-8 / e_k, i.e. a bias of at most 2.8e-8 per even stage.  Round 1 used a degree-12 polynomial
+// in sqrt(w + 2) (one MUFU.SQRT more per call) and before that a deep-tail branch (-4.8 % draws/s).
+#define MC_QUANTILE_POLY(HORNER, t)                                                                               \
+  HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(           \
+      0.01019474611084561f, t, -0.012522037903250294f), t, -0.029537615373728402f), t, 0.05105979421834458f), t, \
+      0.001191401517323608f), t, -0.0434556915527025f), t, 0.04556025718938638f), t, -0.05578006817451819f), t,  \
+      0.059710341538845794f), t, -0.024018910794271674f), t, -0.05160295363704608f), t, 0.17794569832657112f), t, \
+      -0.45756438521357723f), t, 1.9952513929012803f), t, 3.7638425973256995f)
+constexpr float QT_A = -0.08664339756999316f;    // -ln2 / 8
+constexpr float QT_B = -1.1732867951399863f;     // -ln4 / 8 - 1
+
 __device__ __forceinline__ float normal_quantile_fast(float p, float pc) {
-  // w + 2 = -ln2 lg2(p pc) + (2 - 2 ln2) in one FFMA; p pc may flush to 0 (lg2 -> -inf): the clamp holds
-  const float w2 = fminf(fmaf(lg2_approx(p * pc), -0.69314718056f, 0.61370563888f), 18.0f);
-  const float x = sqrt_approx(w2) - 2.82842712474619f;
-  float g = -0.0001458914359425521f;
-  g = fmaf(g, x, 0.00014054195626482066f);
-  g = fmaf(g, x, 0.0012376677239334937f);
-  g = fmaf(g, x, -0.0017637622021570974f);
-  g = fmaf(g, x, -0.0036462519812319317f);
-  g = fmaf(g, x, 0.009457966527136036f);
-  g = fmaf(g, x, -0.0013609513949184736f);
-  g = fmaf(g, x, -0.022852510105916587f);
-  g = fmaf(g, x, 0.04599717902636056f);
-  g = fmaf(g, x, -0.040789581299890895f);
-  g = fmaf(g, x, -0.018363709814932894f);
-  g = fmaf(g, x, 1.59782737417905f);
-  g = fmaf(g, x, 3.2334928032079135f);
-  return g * (p - pc);
+  // p pc may flush to 0 (lg2 -> -inf, t -> +inf): the clamp holds
+  const float t = fminf(fmaf(lg2_approx(p * pc), QT_A, QT_B), 1.0f);
+  return MC_QUANTILE_POLY(horner1, t) * (p - pc);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -375,6 +340,7 @@ __device__ __forceinline__ float ind_indicator(const float* x, const float* b) {
 // FSETP.OR ...) on the ALU pipe and one predicated FADD on the FMA pipe (the crossed and CRN kernels)
 template <int N>
 __device__ __forceinline__ void ind_count(const float* x, const float* b, float& cnt) {
+  static_assert(N >= 1 && N <= 4, "ind_count compares at most 4 populations (the crossed and CRN kernels' range)");
   if constexpr (N == 1) {
     asm("{ .reg .pred p; setp.gt.f32 p, %1, %2; @p add.f32 %0, %0, 0f3F800000; }"
         : "+f"(cnt) : "f"(x[0]), "f"(b[0]));
@@ -455,28 +421,18 @@ __device__ __forceinline__ f2x add2(f2x a, f2x b) {
   f2x d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d;
 }
 
-// normal_tail() for a pair: q = Phi(-a) and e = Phi(a) per lane, the same polynomial and the same
-// operation order (the exponent -a^2 + p(t) is formed as -(a a - p(t)) with the coefficients
-// negated, which is the same fp32 result; the minus sign rides on the EX2 operand).
+// normal_tail() for a pair: q = Phi(-x) and e = Phi(x) per lane, the same polynomial and operation order.
+__device__ __forceinline__ f2x horner2(f2x p, f2x x, float c) { return fma2(p, x, bc2(c)); }
+__device__ __forceinline__ f2x horner2(float p, f2x x, float c) { return fma2(bc2(p), x, bc2(c)); }
+
 __device__ __forceinline__ void normal_tail2(f2x a, f2x& q, f2x& e) {
   float a0, a1;
   up2(a, a0, a1);
-  constexpr float K = (float)(0.28284271247461901 / 0.84932180028801904);
-  const f2x t = pk2(rcp_approx(fmaf(fabsf(a0), K, 1.0f)), rcp_approx(fmaf(fabsf(a1), K, 1.0f)));
-  f2x p = fma2(bc2(0.3020209548193252f), t, bc2(-1.3475361161107364f));
-  p = fma2(p, t, bc2(2.173205689641004f));
-  p = fma2(p, t, bc2(-1.4767906809187563f));
-  p = fma2(p, t, bc2(0.6654844086664139f));
-  p = fma2(p, t, bc2(-0.4449553247379003f));
-  p = fma2(p, t, bc2(-0.5735953408558541f));
-  p = fma2(p, t, bc2(-1.4456196577402736f));
-  p = fma2(p, t, bc2(3.1477861996521375f));        // -p(t)
-  const f2x s = fma2(a, a, p);                      // a^2 - p(t) = -(exponent)
-  float s0, s1;
-  up2(s, s0, s1);
-  const f2x ex = pk2(ex2_approx(-s0), ex2_approx(-s1));
-  const f2x qp = mul2(t, ex);                       // Phi(-|a|)
-  const f2x qc = fma2(qp, bc2(-1.0f), bc2(1.0f));   // Phi(|a|)
+  const f2x m = pk2(fminf(fabsf(a0), PHI_CLAMP), fminf(fabsf(a1), PHI_CLAMP));
+  float E0, E1;
+  up2(MC_PHI_POLY(horner2, m), E0, E1);
+  const f2x qp = pk2(ex2_approx(E0), ex2_approx(E1));   // Phi(-|x|)
+  const f2x qc = fma2(qp, bc2(-1.0f), bc2(1.0f));        // Phi(|x|)
   float qp0, qp1, qc0, qc1;
   up2(qp, qp0, qp1);
   up2(qc, qc0, qc1);
@@ -489,23 +445,10 @@ __device__ __forceinline__ void normal_tail2(f2x a, f2x& q, f2x& e) {
 __device__ __forceinline__ f2x normal_quantile_fast2(f2x p, f2x pc) {
   float m0, m1;
   up2(mul2(p, pc), m0, m1);
-  f2x w2 = fma2(pk2(lg2_approx(m0), lg2_approx(m1)), bc2(-0.69314718056f), bc2(0.61370563888f));
-  float w0, w1;
-  up2(w2, w0, w1);
-  const f2x x = add2(pk2(sqrt_approx(fminf(w0, 18.0f)), sqrt_approx(fminf(w1, 18.0f))), bc2(-2.82842712474619f));
-  f2x g = fma2(bc2(-0.0001458914359425521f), x, bc2(0.00014054195626482066f));
-  g = fma2(g, x, bc2(0.0012376677239334937f));
-  g = fma2(g, x, bc2(-0.0017637622021570974f));
-  g = fma2(g, x, bc2(-0.0036462519812319317f));
-  g = fma2(g, x, bc2(0.009457966527136036f));
-  g = fma2(g, x, bc2(-0.0013609513949184736f));
-  g = fma2(g, x, bc2(-0.022852510105916587f));
-  g = fma2(g, x, bc2(0.04599717902636056f));
-  g = fma2(g, x, bc2(-0.040789581299890895f));
-  g = fma2(g, x, bc2(-0.018363709814932894f));
-  g = fma2(g, x, bc2(1.59782737417905f));
-  g = fma2(g, x, bc2(3.2334928032079135f));
-  return mul2(g, fma2(pc, bc2(-1.0f), p));          // g (p - pc)
+  float t0, t1;
+  up2(fma2(pk2(lg2_approx(m0), lg2_approx(m1)), bc2(QT_A), bc2(QT_B)), t0, t1);
+  const f2x t = pk2(fminf(t0, 1.0f), fminf(t1, 1.0f));
+  return mul2(MC_QUANTILE_POLY(horner2, t), fma2(pc, bc2(-1.0f), p));   // g (p - pc)
 }
 
 // utility_of_b<N, 0, MODEL> for two lanes at once: thresholds b[i] and SOV uniforms vu[k] packed
@@ -538,10 +481,12 @@ __device__ __forceinline__ f2x utility_cond_x2(const f2x* b, const f2x* vu, cons
 
 // Both utilities of a COND record (MODEL 0), packed: sample 0 in the low lane, sample 1 in the high lane.
 // Same words, same normals (pairs consumed in word order, cos first; sample h's normals at nrm + hP),
-// same stage order as utility_of_b<N, 0, 0>.
-template <int N>
+// same stage order as utility_of_b<N, 0, 0>.  This is the fused kernel's COND code; with DBG (the
+// mc_draw_dump test hook) it also writes, per sample h, its unscaled normals, b and u to dbg + h DUMP.
+template <int N, bool DBG = false>
 __device__ __forceinline__ void record_utility_cond_x2(const uint32_t* w, uint32_t one, const float* zc,
-                                                       const ProbRegs<N>& pr, float* u) {
+                                                       const ProbRegs<N>& pr, float* u, float* dbg = nullptr,
+                                                       const float* bsc = nullptr) {
   using G = Geo<N, 0, 0>;
   constexpr int P = G::P, NE = G::NE;
   // Box-Muller (box_muller_scaled) with the radius and angle FFMAs of two word pairs packed
@@ -589,6 +534,25 @@ __device__ __forceinline__ void record_utility_cond_x2(const uint32_t* w, uint32
     vu[k] = add2(pk2(word_to_f12(w[2 * P + k], one), word_to_f12(w[2 * P + NE + k], one)),
                  bc2(-0.99999994039535522f));
   up2(utility_cond_x2<N>(b, vu, pr), u[0], u[1]);
+  if constexpr (DBG) {
+    constexpr int DUMP = G::DUMP;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      float e0, e1;
+      up2(E[j], e0, e1);
+      dbg[j] = e0 * BM_K;
+      dbg[DUMP + j] = e1 * BM_K;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      float b0, b1;
+      up2(b[i], b0, b1);
+      dbg[P + i] = b0 / bsc[i];
+      dbg[DUMP + P + i] = b1 / bsc[i];
+    }
+    dbg[P + N] = u[0];
+    dbg[DUMP + P + N] = u[1];
+  }
 }
 
 // Independent draws: the R utilities of one record, b formed directly from zc (FFMA chains seeded
@@ -600,11 +564,12 @@ __device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, 
                                                const float* bsc = nullptr) {
   using G = Geo<N, EST, MODEL>;
 #if MC_F32X2
-  if constexpr (EST == 0 && MODEL == 0 && !DBG) {
-    record_utility_cond_x2<N>(w, one, zc, pr, u);
+  // COND: the packed pair.  The DBG instantiation (mc_draw_dump) runs this same code and dumps from it.
+  if constexpr (EST == 0 && MODEL == 0) {
+    record_utility_cond_x2<N, DBG>(w, one, zc, pr, u, dbg, bsc);
     return;
   }
-  if constexpr (EST == 0 && MODEL == 1 && !DBG) {   // C4 strata prior: b per sample, the SOV packed
+  if constexpr (EST == 0 && MODEL == 1) {   // C4 strata prior: b per sample, the SOV packed
     float nrm[2 * G::NPAIR];
     record_normals<N, EST, MODEL>(w, one, nrm);
     Shared<N, EST, MODEL> sh0, sh1;
@@ -616,6 +581,19 @@ __device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, 
 #pragma unroll
     for (int k = 0; k < G::NE; ++k) vu[k] = pk2(sh0.vu[k], sh1.vu[k]);
     up2(utility_cond_x2<N>(b, vu, pr), u[0], u[1]);
+    if constexpr (DBG) {
+#pragma unroll
+      for (int k = 0; k < 2 * G::P; ++k) dbg[(k / G::P) * G::DUMP + k % G::P] = nrm[k] * BM_K;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        float b0, b1;
+        up2(b[i], b0, b1);
+        dbg[G::P + i] = b0 / bsc[i];
+        dbg[G::DUMP + G::P + i] = b1 / bsc[i];
+      }
+      dbg[G::P + N] = u[0];
+      dbg[G::DUMP + G::P + N] = u[1];
+    }
     return;
   }
 #endif

@@ -97,8 +97,8 @@ namespace mci {
 mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64_t E, cudaStream_t st,
                        int64_t* sums);
 mc_status launch_finalize(mc_ctx* c, const int64_t* sums, uint64_t N, double* mean, double* var, cudaStream_t st);
-mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64_t* word, int64_t count,
-                             uint32_t* out, cudaStream_t st);
+mc_status launch_philox_dump(uint64_t seed, uint32_t tag, int form, const uint32_t* id, const uint64_t* word,
+                             int64_t count, uint32_t* out, cudaStream_t st);
 mc_status launch_draw_dump(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
                            cudaStream_t st);
 int draw_dump_stride(int n, int est, int model);

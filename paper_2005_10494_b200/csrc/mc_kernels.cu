@@ -553,26 +553,51 @@ mc_status launch_finalize(mc_ctx* c, const int64_t* sums, uint64_t N, double* me
 }
 
 // ---------------------------------------------------------------------------------------------
-// K3: Philox words (test hook).
-__global__ void k_philox_dump(uint64_t seed, const uint32_t* __restrict__ design, const uint64_t* __restrict__ word,
-                              int64_t count, uint32_t* __restrict__ out) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < count) out[i] = philox_word(seed, design[i], word[i]);
+// K3: Philox words (test hook) in the forms the kernels generate them.  Word w of stream (id, tag) is
+// lane w mod 4 of the block with counter (q_lo, q_hi, id, tag), q = w / 4, key (seed_lo, seed_hi):
+//   form 0: philox_block_lo — the fused and CRN kernels' steady state (round keys from the constant
+//           bank, round 1 with the design product hoisted and c0 = hi(M1 id) ^ q_hi ^ k0 held fixed);
+//   form 1: philox_block_rk — the fused kernel's masked (partial-tile / counter-wrap) path (tag 0 only);
+//   form 2: philox_word_tagged — the plain 10-round form of the crossed kernel.
+__device__ __forceinline__ uint32_t word_form(uint64_t seed, const RoundKeys& rk, uint32_t id, uint32_t tag, int form,
+                                              uint64_t w) {
+  const uint64_t q = w >> 2;
+  const uint32_t lo1d = 0xCD9E8D57u * id, hi1d = __umulhi(0xCD9E8D57u, id);
+  uint32_t o[4];
+  if (form == 0)
+    philox_block_lo((uint32_t)q, hi1d ^ (uint32_t)(q >> 32) ^ rk.k0[0], lo1d, rk.k1[0] ^ tag, rk, o);
+  else if (form == 1)
+    philox_block_rk(q, lo1d, hi1d, rk, o);
+  else
+    return philox_word_tagged(seed, id, tag, w);
+  return o[w & 3];
 }
 
-mc_status launch_philox_dump(uint64_t seed, const uint32_t* design, const uint64_t* word, int64_t count, uint32_t* out,
-                             cudaStream_t st) {
+__global__ void k_philox_dump(uint64_t seed, const RoundKeys rk, uint32_t tag, int form, const uint32_t* __restrict__ id,
+                              const uint64_t* __restrict__ word, int64_t count, uint32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < count) out[i] = word_form(seed, rk, id[i], tag, form, word[i]);
+}
+
+mc_status launch_philox_dump(uint64_t seed, uint32_t tag, int form, const uint32_t* id, const uint64_t* word,
+                             int64_t count, uint32_t* out, cudaStream_t st) {
+  if (form < 0 || form > 2 || (form == 1 && tag != 0)) {
+    set_error("mc_philox_dump: form must be 0, 1 (tag 0 only) or 2");
+    return MC_ERR_INVALID;
+  }
   if (count <= 0) return MC_OK;
-  k_philox_dump<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(seed, design, word, count, out);
+  k_philox_dump<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(seed, round_keys(seed), tag, form, id, word, count, out);
   MC_CUDA(cudaGetLastError());
   return MC_OK;
 }
 
-// Per-draw dump through the fused kernel's record_utility (test hook).
+// Per-draw dump through the fused kernel's record_utility (test hook): the words of the sample's record
+// in the steady-state form (philox_block_lo), then the same record code as K1 (COND: the packed pair).
 template <int N, int EST, int MODEL, bool CRN>
 __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restrict__ zc_all,
-                            const int32_t* __restrict__ pod, uint64_t seed, const int64_t* __restrict__ design,
-                            const uint64_t* __restrict__ sample, int64_t count, float* __restrict__ out) {
+                            const int32_t* __restrict__ pod, uint64_t seed, const RoundKeys rk,
+                            const int64_t* __restrict__ design, const uint64_t* __restrict__ sample, int64_t count,
+                            float* __restrict__ out) {
   using G = Geo<N, EST, MODEL>;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= count) return;
@@ -588,23 +613,24 @@ __global__ void k_draw_dump(const float* __restrict__ prob, const float* __restr
   const uint64_t base = G::word_of(sample[i] - sample[i] % G::R);
   const int h = (int)(sample[i] % G::R);
   for (int k = 0; k < G::WR; ++k)
-    w[k] = CRN ? philox_word_tagged(seed, (uint32_t)pod[d], 1u, base + k) : philox_word(seed, (uint32_t)d, base + k);
+    w[k] = word_form(seed, rk, CRN ? (uint32_t)pod[d] : (uint32_t)d, CRN ? 1u : 0u, 0, base + k);
   float bsc[N];
   for (int k = 0; k < N; ++k) bsc[k] = prob[(int64_t)pod[d] * PROB_STRIDE + OFF_BSC + k];
   float u[G::R], dbg[G::R * G::DUMP];
-  record_utility<N, EST, true, MODEL>(w, 0x3F800000u, zc, pr, &sr, u, dbg, bsc);
+  record_utility<N, EST, true, MODEL>(w, one_bits_reg(), zc, pr, &sr, u, dbg, bsc);
   for (int k = 0; k < G::DUMP; ++k) out[i * G::DUMP + k] = dbg[h * G::DUMP + k];
 }
 
 template <int N, int EST, int MODEL = 0>
 static cudaError_t launch_dump_t(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
                                  cudaStream_t st) {
+  const RoundKeys rk = round_keys(c->seed);
   if (c->sampling == 1)
-    k_draw_dump<N, EST, MODEL, true><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod,
-                                                                                   c->seed, design, sample, count, out);
+    k_draw_dump<N, EST, MODEL, true><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(
+        c->d_prob, c->d_zc, c->d_pod, c->seed, rk, design, sample, count, out);
   else
-    k_draw_dump<N, EST, MODEL, false><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(c->d_prob, c->d_zc, c->d_pod,
-                                                                                    c->seed, design, sample, count, out);
+    k_draw_dump<N, EST, MODEL, false><<<(unsigned)((count + 127) / 128), 128, 0, st>>>(
+        c->d_prob, c->d_zc, c->d_pod, c->seed, rk, design, sample, count, out);
   return cudaGetLastError();
 }
 

@@ -86,7 +86,7 @@ def lib() -> ctypes.CDLL:
         L.mc_num_designs.argtypes = [vp]; L.mc_num_designs.restype = i64
         L.mc_num_problems.argtypes = [vp]; L.mc_num_problems.restype = i32
         L.mc_words_per_draw.argtypes = [vp]; L.mc_words_per_draw.restype = i32
-        L.mc_philox_dump.argtypes = [u64, vp, vp, i64, vp, vp]; L.mc_philox_dump.restype = i32
+        L.mc_philox_dump.argtypes = [u64, ctypes.c_uint32, i32, vp, vp, i64, vp, vp]; L.mc_philox_dump.restype = i32
         L.mc_draw_dump.argtypes = [vp, vp, vp, i64, vp, vp]; L.mc_draw_dump.restype = i32
         L.mc_draw_dump_stride.argtypes = [vp]; L.mc_draw_dump_stride.restype = i32
         L.mc_kernel_launches.argtypes = [vp]; L.mc_kernel_launches.restype = i64
@@ -204,13 +204,18 @@ def candidates(problems, m: int = 64, n3: int = 0, seed: int = 0, device: int = 
     return A[:D], pod[:D]
 
 
-def philox_dump(seed: int, design, word, stream=None):
-    """K3: Philox words for (design, word-index) pairs (device tensors in, device tensor out)."""
+PHILOX_FORM_STEADY, PHILOX_FORM_MASKED, PHILOX_FORM_PLAIN = 0, 1, 2
+
+
+def philox_dump(seed: int, design, word, tag: int = 0, form: int = PHILOX_FORM_STEADY, stream=None):
+    """K3: Philox words of stream (id, tag) for (id, word-index) pairs, in the block form `form` the kernels
+    use (device tensors in, device tensor out)."""
     torch = _torch()
     design = design.to(torch.int32).contiguous()
     word = word.to(torch.int64).contiguous()
     out = torch.empty(design.numel(), dtype=torch.int32, device=design.device)
-    _check(lib().mc_philox_dump(seed, design.data_ptr(), word.data_ptr(), design.numel(), out.data_ptr(), _stream(stream)))
+    _check(lib().mc_philox_dump(seed, tag, form, design.data_ptr(), word.data_ptr(), design.numel(), out.data_ptr(),
+                                _stream(stream)))
     return out
 
 
@@ -281,6 +286,17 @@ class Design:
     def set_launch(self, block_threads: int = 0, grid_blocks: int = 0):
         _check(lib().mc_set_launch(self._ctx, block_threads, grid_blocks))
 
+    def _check_sums(self, sums, where: str):
+        """The sums buffer the kernels' 64-bit atomics write: a contiguous int64 (D, 2) CUDA tensor on the
+        ctx device (anything else would be written past its end or into the wrong elements)."""
+        torch = _torch()
+        if not (isinstance(sums, torch.Tensor) and sums.is_cuda and sums.dtype == torch.int64
+                and sums.is_contiguous() and tuple(sums.shape) == (self.D, 2)
+                and sums.device.index == self.device):
+            raise ValueError(f"{where}: sums must be a contiguous int64 CUDA tensor of shape ({self.D}, 2) on "
+                             f"cuda:{self.device}; got {getattr(sums, 'dtype', type(sums))} "
+                             f"{tuple(getattr(sums, 'shape', ()))} on {getattr(sums, 'device', '?')}")
+
     def new_sums(self):
         torch = _torch()
         return torch.zeros((self.D, 2), dtype=torch.int64, device=f"cuda:{self.device}")
@@ -290,18 +306,20 @@ class Design:
         """Rows a2-a6: accumulate the integer sums of samples [begin, begin+count) into `sums`."""
         if design_count is None:
             design_count = self.D - design_begin
-        assert sums.is_cuda and sums.dtype.is_floating_point is False and sums.numel() == 2 * self.D
+        self._check_sums(sums, "evaluate")
         _check(lib().mc_evaluate_grid(self._ctx, design_begin, design_count, sample_begin, sample_count,
                                       _stream(stream), sums.data_ptr()))
         return sums
 
     def evaluate_crossed(self, sums, n1: int, n2: int, stream=None):
         """NEXT f3 (ii): the paper's crossed N1 x N2 estimator (ctx built with EST_IND)."""
+        self._check_sums(sums, "evaluate_crossed")
         _check(lib().mc_evaluate_crossed(self._ctx, n1, n2, _stream(stream), sums.data_ptr()))
         return sums
 
     def finalize_crossed(self, sums, n1: int, n2: int, stream=None):
         torch = _torch()
+        self._check_sums(sums, "finalize_crossed")
         mean = torch.empty(self.D, dtype=torch.float64, device=sums.device)
         var = torch.empty(self.D, dtype=torch.float64, device=sums.device)
         _check(lib().mc_finalize_crossed(self._ctx, sums.data_ptr(), n1, n2, mean.data_ptr(), var.data_ptr(),
@@ -311,6 +329,7 @@ class Design:
     def finalize(self, sums, total_samples: int, stream=None):
         """Row a8: per-design mean and per-draw variance (fp64 tensors)."""
         torch = _torch()
+        self._check_sums(sums, "finalize")
         mean = torch.empty(self.D, dtype=torch.float64, device=sums.device)
         var = torch.empty(self.D, dtype=torch.float64, device=sums.device)
         _check(lib().mc_finalize(self._ctx, sums.data_ptr(), total_samples, mean.data_ptr(), var.data_ptr(),

@@ -60,6 +60,9 @@ def test_empty_and_single_sample_calls(O, mc, torch):
     with pytest.raises(mc.McError):
         dsg.evaluate(s, 2**40, 1)               # beyond the int64 headroom of 2^40 draws per design
     with pytest.raises(mc.McError):
+        dsg.evaluate(s, 2**40 - 1, 1)           # exactly 2^40 sample indices: 2^40 x 2^23 = 2^63 overflows
+    dsg.evaluate(s, 2**40 - 2, 1)               # the last admissible sample index
+    with pytest.raises(mc.McError):
         dsg.evaluate(s, 0, 10, design_begin=1, design_count=5)
     with pytest.raises(mc.McError):
         dsg.set_launch(48, 0)                   # not a multiple of 32
@@ -141,3 +144,34 @@ def test_checkpoint_resume_is_bit_identical(O, mc, torch, tmp_path):
     resumed = torch.from_numpy(s).cuda()
     dsg.evaluate(resumed, done, 300_001 - done)
     assert seed == SEED and torch.equal(resumed, full)
+
+
+def test_sums_buffer_is_validated(mc, torch):
+    """The 64-bit atomics write sums[2d], sums[2d+1]: any buffer other than a contiguous int64 (D, 2) CUDA
+    tensor on the ctx device is rejected before a kernel runs."""
+    spec = W.c2_slice()
+    alpha = np.array([[0.0025, 0.0138, 0.0128], [0.01, 0.005, 0.0123]])
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, np.zeros(2, dtype=np.int32), seed=SEED)
+    bad = [torch.zeros((2, 2), dtype=torch.int32, device="cuda"),          # int32: atomics would overrun
+           torch.zeros((2, 4), dtype=torch.int64, device="cuda")[:, ::2],  # non-contiguous view
+           torch.zeros((4,), dtype=torch.int64, device="cuda"),            # right numel, wrong shape
+           torch.zeros((2, 2), dtype=torch.int64)]                         # host tensor
+    for s in bad:
+        with pytest.raises(ValueError):
+            dsg.evaluate(s, 0, 10)
+        with pytest.raises(ValueError):
+            dsg.finalize(s, 10)
+    dsg.close()
+
+
+def test_crossed_rejects_int64_overflow(mc, torch):
+    """S2 = sum_k c_k^2 <= N1 N2^2 must fit int64: N1 N2^2 >= 2^63 is rejected up front."""
+    spec = W.c2_slice()
+    dsg = mc.Design([lib_problem(mc, spec)], np.array([[0.0025, 0.0138, 0.0128]]), np.zeros(1, dtype=np.int32),
+                    seed=SEED, estimator=mc.EST_IND)
+    s = dsg.new_sums()
+    with pytest.raises(mc.McError):
+        dsg.evaluate_crossed(s, 2**31, 2**16)          # exactly 2^63
+    dsg.evaluate_crossed(s, 1000, 2**16)               # fine
+    assert int(s[0, 0]) > 0
+    dsg.close()

@@ -36,15 +36,28 @@ def _oracle_sums(O, oprob, alpha, est, design, s0, count):
 
 
 # ----------------------------------------------------------------------------------------------
-def test_philox_words_bit_exact(O, mc, torch):
-    rng = np.random.default_rng(0)
-    designs = np.concatenate([rng.integers(0, 2**31, 200), [0, 1, 2**32 - 1]]).astype(np.uint32)
-    words = np.concatenate([rng.integers(0, 2**40, 200), [0, 4 * 2**32 + 5, 2**62]]).astype(np.uint64)
+@pytest.mark.parametrize("tag,form", [(0, 0), (0, 1), (0, 2), (1, 0), (1, 2), (2, 2), (3, 2)])
+def test_philox_words_bit_exact(O, mc, torch, tag, form):
+    """Every block form the kernels use (0: fused/CRN steady state with round 1 hoisted and constant-bank
+    round keys; 1: the fused kernel's masked path; 2: the crossed kernel's plain rounds), on every stream
+    tag, bit-exact against the oracle's textbook Philox4x32-10 — including q_hi != 0 and ids up to 2^32-1."""
+    rng = np.random.default_rng(tag * 3 + form)
+    designs = np.concatenate([rng.integers(0, 2**32, 300), [0, 1, 2**32 - 1]]).astype(np.uint32)
+    words = np.concatenate([rng.integers(0, 2**40, 150), rng.integers(4 * 2**32 - 64, 4 * 2**32 + 64, 150),
+                            [0, 4 * 2**32 + 5, 2**62]]).astype(np.uint64)
     out = mc.philox_dump(SEED, torch.tensor(designs.astype(np.int64)).to(torch.int32).cuda(),
-                         torch.tensor(words.astype(np.int64)).cuda())
+                         torch.tensor(words.astype(np.int64)).cuda(), tag=tag, form=form)
     got = out.cpu().numpy().view(np.uint32)
-    ref = np.array([O.word(SEED, int(d), int(w)) for d, w in zip(designs, words)], dtype=np.uint32)
+    ref = np.array([O.word_tagged(SEED, int(d), tag, int(w)) for d, w in zip(designs, words)], dtype=np.uint32)
     assert np.array_equal(got, ref)
+
+
+def test_philox_dump_rejects_bad_form(mc, torch):
+    d = torch.zeros(1, dtype=torch.int32).cuda()
+    w = torch.zeros(1, dtype=torch.int64).cuda()
+    for tag, form in [(1, 1), (0, 3), (0, -1)]:
+        with pytest.raises(mc.McError):
+            mc.philox_dump(SEED, d, w, tag=tag, form=form)
 
 
 @pytest.mark.parametrize("est", [0, 1])
@@ -53,8 +66,10 @@ def test_per_draw_parity(O, mc, torch, est):
     specs, alpha, pod = c1_workload(O)
     dsg = mc.Design([lib_problem(mc, s) for s in specs], alpha, pod, seed=SEED, estimator=est)
     rng = np.random.default_rng(1)
-    D = rng.integers(0, len(specs), 400)
-    S = np.concatenate([rng.integers(0, 10**6, 396), [0, 1, 2**33 + 1, 10**12]])
+    # thousands of draws; both samples of many COND records (2j, 2j+1): the dump runs K1's packed pair
+    pairs = rng.integers(0, 5 * 10**5, 600) * 2
+    D = rng.integers(0, len(specs), 2404)
+    S = np.concatenate([pairs, pairs + 1, rng.integers(0, 10**6, 1200), [0, 1, 2**33 + 1, 10**12]])
     rec = dsg.draw_dump(torch.tensor(D).cuda(), torch.tensor(S).cuda()).cpu().numpy().astype(np.float64)
     n = 2
     nn = n if est == 0 else 2 * n
@@ -201,6 +216,28 @@ def test_sample_subrange_parity_beyond_2_32(O, mc, torch):
             assert abs(got[d] - ref) <= REL * ref
 
 
+@pytest.mark.parametrize("est,wrap", [(0, 2**32), (1, 2863311530)])
+def test_sums_across_philox_counter_wrap(O, mc, torch, est, wrap):
+    """The steady-state loop advances a 32-bit block counter with q_hi held fixed and falls back to the
+    64-bit masked form when a thread's run would cross q_lo = 2^32 (mc_kernels.cu run_samples).  Sample
+    ranges around that wrap (COND n = 3: q = s; IND n = 3: q = 1.5 s, so runs straddle it) match the
+    oracle: COND within 1e-5 relative, IND bit-exact up to near-tie flips."""
+    spec, alpha = slice_designs(O, m=64, count=3, seed=5)
+    pod = np.zeros(len(alpha), dtype=np.int32)
+    dsg = mc.Design([lib_problem(mc, spec)], alpha, pod, seed=SEED, estimator=est)
+    op = oracle_problem(O, spec)
+    s0, cnt = wrap - 3000, 6000
+    sums = dsg.new_sums()
+    dsg.evaluate(sums, s0, cnt)
+    got = sums.cpu().numpy()
+    for d in range(len(alpha)):
+        ref = _oracle_sums(O, op, alpha[d], est, d, s0, cnt)
+        if est == 0:
+            assert abs(got[d, 0] - ref[0]) <= REL * ref[0], (d, got[d], ref)
+        else:
+            assert abs(int(got[d, 0]) - int(ref[0])) <= 2 * 2**23
+
+
 def test_point_mass_n1_exact_on_gpu(O, mc, torch):
     """Point mass, n = 1, exact Eq.-9 I3: every draw's u = 1 - beta = 0.9 (fp32 Phi accuracy)."""
     i3 = mc.information_units(0.025, 0.1, 0.25)
@@ -282,11 +319,11 @@ def test_dimension_sweep_parity(O, mc, torch, n, est):
             assert abs(got[d] - ref) <= REL * ref, (n, d, got[d], ref)
         else:
             assert abs(int(sums[d, 0].item()) - int(ref_s[0])) // 2**23 <= 2
-    # per-draw records for the same designs
-    D = torch.tensor([0, len(alpha) - 1] * 16).cuda()
-    S = torch.arange(32).cuda() * 7919
+    # per-draw records for the same designs (512 draws: both halves of COND records, K1's packed code)
+    D = torch.tensor([0, len(alpha) - 1] * 256).cuda()
+    S = (torch.arange(512).cuda() // 2) * 7919 * 2 + torch.arange(512).cuda() % 2
     rec = dsg.draw_dump(D, S).cpu().numpy()
-    for i in range(32):
+    for i in range(512):
         o = O.draw(op, alpha[int(D[i])], est, SEED, int(D[i]), int(S[i]))
         if est == 0:
             assert abs(rec[i, -1] - o["u"]) <= 5e-5
@@ -323,8 +360,8 @@ def test_c4_strata_prior_parity(O, mc, torch, est):
         else:
             flips += abs(int(sums[d, 0].item()) - int(ref_s[0])) // 2**23
     assert flips <= 2
-    D = torch.tensor(list(range(len(alpha))) * 4).cuda()
-    S = torch.arange(4 * len(alpha)).cuda() * 104729 + 3
+    D = torch.tensor(list(range(len(alpha))) * 60).cuda()
+    S = torch.arange(60 * len(alpha)).cuda() * 104729 + 3
     rec = dsg.draw_dump(D, S).cpu().numpy().astype(np.float64)
     for i in range(len(D)):
         d = int(D[i])
@@ -497,7 +534,7 @@ def test_inverse_cdf_clamp_region(O, mc, torch):
     S = np.arange(0, 4000, dtype=np.int64) * 7919 + 1
     rec = dsg.draw_dump(torch.zeros(len(S), dtype=torch.int64).cuda(), torch.tensor(S).cuda()).cpu().numpy()
     op = O.point_mass_problem(r, theta, i3)
-    for i, s in enumerate(S[:400]):
+    for i, s in enumerate(S[:2000]):
         o = O.draw(op, a, 0, SEED, 0, int(s))
         assert abs(float(rec[i, -1]) - o["u"]) <= 1.5e-7, (s, rec[i, -1], o["u"])
     N = 400_000

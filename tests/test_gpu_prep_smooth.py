@@ -24,16 +24,52 @@ def mc(torch):
     return m
 
 
-@pytest.mark.parametrize("r", [[1.0], [1.0, 0.3], [1.0, 0.45, 0.15], [1.0, 0.95, 0.9], [1.0, 0.8, 0.6, 0.4, 0.2]])
+C5_R10 = [(10 - i) / 10 for i in range(10)]
+
+
+@pytest.mark.parametrize("r", [[1.0], [1.0, 0.3], [1.0, 0.45, 0.15], [1.0, 0.95, 0.9], [1.0, 0.8, 0.6, 0.4, 0.2],
+                               [1.0, 0.6, 0.35, 0.15], [1.0, 0.99, 0.98, 0.97], C5_R10])
 def test_fwer_matches_oracle(O, mc, r):
+    """K4 FWER (n <= 3: one thread per point; n >= 4: the forward chain recursion, one CTA per point) against
+    the oracle's backward transfer quadrature (a different rule: numpy's 20-point Gauss-Legendre)."""
     n = len(r)
     spec_p = mc.problem_formula10(r, [0.25] * n, 211.0)
     rng = np.random.default_rng(n)
-    A = rng.uniform(0, 0.012, size=(12, n))
+    A = rng.uniform(0, 0.012, size=(6 if n >= 10 else 12, n))
     A[0, -1] = 0.0            # alpha = 0 -> z = +inf
     got = mc.fwer(spec_p, A)
     ref = np.array([O.fwer(r, a) for a in A])
-    assert np.allclose(got, ref, rtol=0, atol=2e-12 if n <= 3 else 2e-8)
+    assert np.allclose(got, ref, rtol=0, atol=2e-12)
+
+
+def test_fwer_n4_close_ratios_is_resolved(O, mc):
+    """for n >= 4 the panels follow the narrowest conditional sd (r ratios 0.999: s = 0.032).  The
+    FWER of highly correlated tests lies in [max alpha_i, sum alpha_i] and matches the oracle."""
+    r = [1.0, 0.999, 0.998, 0.997]
+    A = np.array([[0.006] * 4, [0.002, 0.004, 0.006, 0.001], [0.0, 0.0, 0.0, 0.006]])
+    got = mc.fwer(mc.problem_formula10(r, [0.25] * 4, 211.0), A)
+    for a, g in zip(A, got):
+        assert a.max() - 1e-12 <= g <= a.sum() + 1e-12
+    ref = np.array([O.fwer(r, a) for a in A])
+    assert np.allclose(got, ref, rtol=0, atol=2e-12)
+    assert got[2] == pytest.approx(0.006, abs=1e-12)          # only the last test can reject
+
+
+def test_candidates_n4_close_ratios(O, mc):
+    """alpha_4 solved on the GPU for closely spaced r makes the oracle's FWER equal alpha0."""
+    r = [1.0, 0.99, 0.98, 0.97]
+    A, _ = mc.candidates([mc.problem_formula10(r, [0.25] * 4, 211.0)], m=4, n3=0, seed=W.SEED)
+    assert len(A) > 0
+    for a in A[:: max(1, len(A) // 4)]:
+        assert O.fwer(r, a) == pytest.approx(0.025, abs=1e-11)
+
+
+def test_chain_rejects_unresolvable_ratio(mc):
+    """n >= 4 with r ratios so close to 1 that a level would need more than the node cap: MC_ERR_NUMERIC."""
+    p = mc.problem_formula10([1.0, 1 - 1e-5, 1 - 2e-5, 1 - 3e-5], [0.25] * 4, 211.0)
+    with pytest.raises(mc.McError) as e:
+        mc.fwer(p, np.full((1, 4), 0.005))
+    assert e.value.status == 2
 
 
 def test_candidates_grid_matches_oracle(O, mc):
