@@ -100,6 +100,14 @@ mc_status mc_problem_strata(double r2, double i3, double alpha0, const double* s
 mc_status mc_fwer(const mc_problem* p, const double* alpha_host, int64_t count, double* fwer_host,
                   int32_t cuda_device);
 
+/* alpha_n of explicit partial designs (Sec. 2.1 re-parametrisation; Formula 2): for each of
+ * `count` rows of alpha_host[count*n] (row-major; alpha_1..alpha_{n-1} given, in [0, alpha0]) of problem
+ * problem_host[count] (index into probs[n_probs], all sharing n), solves FWER(alpha_1..alpha_n) = alpha0 for
+ * alpha_n in [0, alpha0] on the GPU (fp64) and writes it into the row; valid_host[count] =
+ * 1 if feasible, 0 if FWER(.., 0) > alpha0 (row's alpha_n = NaN).  Host buffers; synchronises. */
+mc_status mc_solve_alpha_n(const mc_problem* probs, int32_t n_probs, const int32_t* problem_host,
+                           int64_t count, double* alpha_host, uint8_t* valid_host, int32_t cuda_device);
+
 /* Candidate designs for n_probs problems sharing n: the half-offset m^(n-1) grid on
  * (0, alpha0)^(n-1) (first coordinate slowest), alpha_n solved from Formula 2 on the GPU (fp64,
  * one thread per grid point), infeasible points dropped; then, if 0 < n3 < #valid, the seeded

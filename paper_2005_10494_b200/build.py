@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stdout + r.stderr)
             if r.returncode != 0:
                 raise subprocess.CalledProcessError(r.returncode, c)
-        link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out, *objs, "-lcusolver", "-lcublas"]
+        link = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out, *objs, "-lcusolver"]
         subprocess.check_call(link)
     return LIB
 

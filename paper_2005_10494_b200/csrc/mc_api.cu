@@ -525,6 +525,30 @@ mc_status mc_fwer(const mc_problem* p, const double* alpha, int64_t count, doubl
   return fwer_eval(p, alpha, count, out, device);
 }
 
+mc_status mc_solve_alpha_n(const mc_problem* probs, int32_t n_probs, const int32_t* prob, int64_t count,
+                           double* alpha, uint8_t* valid, int32_t device) {
+  NvtxRange _nvtx("mc_solve_alpha_n");
+  if (!probs || n_probs <= 0 || (count > 0 && (!prob || !alpha || !valid))) {
+    set_error("mc_solve_alpha_n: null pointer or no problems");
+    return MC_ERR_INVALID;
+  }
+  const int n = probs[0].n;
+  for (int k = 0; k < n_probs; ++k) {
+    mc_status s = validate_problem(probs[k], k);
+    if (s != MC_OK) return s;
+    if (probs[k].n != n) { set_error("mc_solve_alpha_n: all problems must share n"); return MC_ERR_INVALID; }
+  }
+  for (int64_t t = 0; t < count; ++t) {
+    if (prob[t] < 0 || prob[t] >= n_probs) { set_error("mc_solve_alpha_n: problem index out of range"); return MC_ERR_INVALID; }
+    for (int i = 0; i + 1 < n; ++i)
+      if (!(alpha[t * n + i] >= 0.0 && alpha[t * n + i] <= probs[prob[t]].alpha0)) {
+        set_error("mc_solve_alpha_n: alpha_1..alpha_{n-1} must lie in [0, alpha0]");
+        return MC_ERR_INVALID;
+      }
+  }
+  return alpha_points_solve(probs, n_probs, prob, count, device, alpha, valid);
+}
+
 mc_status mc_candidates(const mc_problem* probs, int32_t n_probs, int32_t m, int64_t n3, uint64_t seed,
                         double* alpha_out, int32_t* problem_out, int64_t cap, int64_t* n_out, int32_t device) {
   NvtxRange _nvtx("mc_candidates");

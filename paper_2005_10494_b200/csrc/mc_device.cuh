@@ -451,6 +451,40 @@ __device__ __forceinline__ f2x normal_quantile_fast2(f2x p, f2x pc) {
   return mul2(MC_QUANTILE_POLY(horner2, t), fma2(pc, bc2(-1.0f), p));   // g (p - pc)
 }
 
+// Lane-split forms: the same per-lane operations as normal_tail2 / normal_quantile_fast2 (bit-identical
+// results) issued as scalar FFMAs.  A packed FFMA2 occupies BOTH the fmaheavy and fmalite datapaths for
+// two cycles, while a scalar FFMA takes one of them; IMAD.WIDE (Philox) needs fmaheavy for four cycles.
+// Moving part of the polynomial work to scalar FFMAs lets the scheduler run it on fmalite while fmaheavy
+// is busy with Philox products (profiles/r02/pipe_model.md).
+#ifndef MC_SCALAR_PHI_EVEN
+#define MC_SCALAR_PHI_EVEN 0
+#endif
+#ifndef MC_SCALAR_PHI_ODD
+#define MC_SCALAR_PHI_ODD 0
+#endif
+#ifndef MC_SCALAR_QUANTILE
+#define MC_SCALAR_QUANTILE 0
+#endif
+__device__ __forceinline__ void normal_tail2s(f2x a, f2x& q, f2x& e) {
+  float a0, a1, q0, q1, e0, e1;
+  up2(a, a0, a1);
+  normal_tail(a0, q0, e0);
+  normal_tail(a1, q1, e1);
+  q = pk2(q0, q1);
+  e = pk2(e0, e1);
+}
+__device__ __forceinline__ f2x normal_quantile_fast2s(f2x p, f2x pc) {
+  float p0, p1, c0, c1;
+  up2(p, p0, p1);
+  up2(pc, c0, c1);
+  return pk2(normal_quantile_fast(p0, c0), normal_quantile_fast(p1, c1));
+}
+template <bool SCALAR>
+__device__ __forceinline__ void normal_tail2x(f2x a, f2x& q, f2x& e) {
+  if constexpr (SCALAR) normal_tail2s(a, q, e);
+  else normal_tail2(a, q, e);
+}
+
 // utility_of_b<N, 0, MODEL> for two lanes at once: thresholds b[i] and SOV uniforms vu[k] packed
 // (two samples of a record, or two designs sharing a sample under common random numbers).
 template <int N>
@@ -461,11 +495,12 @@ __device__ __forceinline__ f2x utility_cond_x2(const f2x* b, const f2x* vu, cons
 #pragma unroll
   for (int k = 0; k < NE; ++k) {
     const f2x a = k == 0 ? b[1] : fma2(bc2(-pr.er[k]), x[k > 0 ? k - 1 : 0], b[2 * k + 1]);
-    normal_tail2(a, q, e);
+    normal_tail2x<MC_SCALAR_PHI_EVEN>(a, q, e);
     uu = k == 0 ? q : fma2(fma2(uu, bc2(-1.0f), bc2(1.0f)), q, uu);
     const f2x v = vu[k];
     const f2x vc = fma2(v, bc2(-1.0f), bc2(1.0f));                            // exact
-    const f2x y = normal_quantile_fast2(mul2(v, e), fma2(v, q, vc));
+    const f2x y = MC_SCALAR_QUANTILE ? normal_quantile_fast2s(mul2(v, e), fma2(v, q, vc))
+                                     : normal_quantile_fast2(mul2(v, e), fma2(v, q, vc));
     x[k] = k == 0 ? y : fma2(bc2(pr.esd[k]), y, mul2(bc2(pr.emu[k]), x[k > 0 ? k - 1 : 0]));
   }
 #pragma unroll
@@ -473,7 +508,7 @@ __device__ __forceinline__ f2x utility_cond_x2(const f2x* b, const f2x* vu, cons
     f2x a = b[2 * j];
     if (2 * j >= 1) a = fma2(bc2(-pr.oa[j]), x[j > 0 ? j - 1 : 0], a);
     if (2 * j + 1 < N) a = fma2(bc2(-pr.ob[j]), x[j < NE ? j : 0], a);
-    normal_tail2(a, q, e);
+    normal_tail2x<MC_SCALAR_PHI_ODD>(a, q, e);
     uu = (NE == 0 && j == 0) ? q : fma2(fma2(uu, bc2(-1.0f), bc2(1.0f)), q, uu);
   }
   return uu;

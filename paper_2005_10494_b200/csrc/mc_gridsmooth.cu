@@ -7,10 +7,10 @@
 // tr S = tr S_r tr S_a, first minimiser with the r bandwidth outer (the oracle's order).
 //
 // Kernels: k_nw_matrix builds all 11 S_x (one block per (row, bandwidth), deterministic tree sums);
-// the two products per bandwidth pair are plain fp64 GEMMs (cuBLAS; 256^3 each for C4), batched over the
-// alpha bandwidths; k_grid_rss reduces ||P^ - P~||^2 per pair in a fixed order (one block per pair), so
-// the GCV choice is deterministic.  All fp64.
-#include <cublas_v2.h>
+// the two products per bandwidth pair are fp64 GEMMs in k_dgemm (this file; 256^3 each for C4, batched
+// over the alpha bandwidths; DFMA on the FP64 pipe — under 1 ms per GCV scan, so no tensor-core path);
+// k_grid_rss reduces ||P^ - P~||^2 per pair in a fixed order (one block per pair), so the GCV choice is
+// deterministic.  All fp64, fixed summation orders.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -70,17 +70,68 @@ __global__ void __launch_bounds__(GS_THREADS) k_grid_rss(const double* __restric
   if (threadIdx.x == 0) rss[blockIdx.x] = red[0];
 }
 
-namespace {
-// One cuBLAS handle per (host thread, device): cublasSetStream on a shared handle would race between
-// threads.  Handles live for the thread (not destroyed at exit: the CUDA context may already be gone).
-thread_local cublasHandle_t t_blas[64] = {};
-
-cublasHandle_t blas_handle(int dev) {
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!t_blas[dev] && cublasCreate(&t_blas[dev]) != CUBLAS_STATUS_SUCCESS) t_blas[dev] = nullptr;
-  return t_blas[dev];
+// C[z] = A[z] op(B[z]) for z = blockIdx.z, row-major: A is M x K (lda), op(B) = B (K x N, ldb) or, with
+// BT, B^T for B stored N x K (ldb); element strides sA, sB, sC between batch entries (0 = shared operand).
+// 64 x 64 output tile per 256-thread block (4 x 4 outputs per thread), K in slabs of 16 through shared
+// memory; each output is one DFMA chain in k order (deterministic).
+constexpr int DG_T = 64, DG_K = 16;
+template <bool BT>
+__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, const double* __restrict__ A, int lda, int64_t sA,
+                                               const double* __restrict__ B, int ldb, int64_t sB, double* __restrict__ C,
+                                               int ldc, int64_t sC) {
+  __shared__ double As[DG_K][DG_T + 1];
+  __shared__ double Bs[DG_K][DG_T + 1];
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+  const int m0 = blockIdx.y * DG_T, n0 = blockIdx.x * DG_T;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += DG_K) {
+    for (int e = threadIdx.x; e < DG_T * DG_K; e += blockDim.x) {
+      const int r = e / DG_K, kk = e % DG_K, gm = m0 + r, gk = k0 + kk;
+      As[kk][r] = (gm < M && gk < K) ? A[(int64_t)gm * lda + gk] : 0.0;
+      if (BT) {
+        const int gn = n0 + r;
+        Bs[kk][r] = (gn < N && gk < K) ? B[(int64_t)gn * ldb + gk] : 0.0;
+      } else {
+        const int kb = e / DG_T, c = e % DG_T, gkb = k0 + kb, gn = n0 + c;
+        Bs[kb][c] = (gkb < K && gn < N) ? B[(int64_t)gkb * ldb + gn] : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < DG_K; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+      if (gm < M && gn < N) C[(int64_t)gm * ldc + gn] = acc[i][j];
+    }
 }
 
+template <bool BT>
+static cudaError_t dgemm(int M, int N, int K, const double* A, int lda, int64_t sA, const double* B, int ldb, int64_t sB,
+                         double* C, int ldc, int64_t sC, int batch, cudaStream_t st) {
+  const dim3 grid((N + DG_T - 1) / DG_T, (M + DG_T - 1) / DG_T, batch);
+  k_dgemm<BT><<<grid, 256, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  return cudaGetLastError();
+}
+
+namespace {
 struct DevBuf {
   void* p = nullptr;
   ~DevBuf() { if (p) cudaFree(p); }
@@ -91,11 +142,7 @@ struct DevBuf {
 
 using namespace mci;
 
-#define MC_BLAS(call)                                                                   \
-  do {                                                                                  \
-    cublasStatus_t _s = (call);                                                         \
-    if (_s != CUBLAS_STATUS_SUCCESS) { set_error("mc_grid_smooth: " #call " failed"); return MC_ERR_CUDA; } \
-  } while (0)
+
 
 extern "C" {
 
@@ -110,12 +157,7 @@ mc_status mc_grid_smooth(const double* values_dev, int32_t nr, int32_t na, const
     if (!(xa_host[i] > xa_host[i - 1])) { set_error("mc_grid_smooth: alpha coordinates must be strictly increasing"); return MC_ERR_INVALID; }
   const bool gcv = !(hr > 0.0) || !(ha > 0.0);
   if (!gcv && (!std::isfinite(hr) || !std::isfinite(ha))) { set_error("mc_grid_smooth: bandwidths must be finite"); return MC_ERR_INVALID; }
-  int dev = 0;
-  MC_CUDA(cudaGetDevice(&dev));
-  cublasHandle_t bh = blas_handle(dev);
-  if (!bh) { set_error("mc_grid_smooth: cublasCreate failed"); return MC_ERR_CUDA; }
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  MC_BLAS(cublasSetStream(bh, st));
 
   const int nh = gcv ? GS_NH : 1;
   std::vector<double> h_r(nh), h_a(nh);
@@ -149,16 +191,13 @@ mc_status mc_grid_smooth(const double* values_dev, int32_t nr, int32_t na, const
   k_nw_matrix<<<dim3(nr, nh), GS_THREADS, 0, st>>>(d_xr, nr, d_hr, d_Sr, d_dr);
   k_nw_matrix<<<dim3(na, nh), GS_THREADS, 0, st>>>(d_xa, na, d_ha, d_Sa, d_da);
   MC_CUDA(cudaGetLastError());
-  const double one = 1.0, zero = 0.0;
-  // row-major X[r][c] is column-major X^T[c][r]:  T = S_r P  <=>  T^T = P^T S_r^T;  Ps = T S_a^T  <=>  Ps^T = S_a T^T
+  // T = S_r P (nr x na), then Ps[ja] = T S_a[ja]^T for every alpha bandwidth (row-major)
   int jr_best = 0, ja_best = 0;
   if (gcv) {
     std::vector<double> dr((size_t)nh * nr), da((size_t)nh * na), rss((size_t)nh * nh);
     for (int jr = 0; jr < nh; ++jr) {
-      MC_BLAS(cublasDgemm(bh, CUBLAS_OP_N, CUBLAS_OP_N, na, nr, nr, &one, values_dev, na,
-                          d_Sr + (size_t)jr * nr * nr, nr, &zero, d_T, na));
-      MC_BLAS(cublasDgemmStridedBatched(bh, CUBLAS_OP_T, CUBLAS_OP_N, na, nr, na, &one, d_Sa, na, (long long)na * na,
-                                        d_T, na, 0, &zero, d_Ps, na, n, nh));
+      MC_CUDA(dgemm<false>(nr, na, nr, d_Sr + (size_t)jr * nr * nr, nr, 0, values_dev, na, 0, d_T, na, 0, 1, st));
+      MC_CUDA(dgemm<true>(nr, na, na, d_T, na, 0, d_Sa, na, (int64_t)na * na, d_Ps, na, n, nh, st));
       k_grid_rss<<<nh, GS_THREADS, 0, st>>>(values_dev, d_Ps, n, d_rss + (size_t)jr * nh);
       MC_CUDA(cudaGetLastError());
     }
@@ -179,10 +218,8 @@ mc_status mc_grid_smooth(const double* values_dev, int32_t nr, int32_t na, const
       }
     }
   }
-  MC_BLAS(cublasDgemm(bh, CUBLAS_OP_N, CUBLAS_OP_N, na, nr, nr, &one, values_dev, na,
-                      d_Sr + (size_t)jr_best * nr * nr, nr, &zero, d_T, na));
-  MC_BLAS(cublasDgemm(bh, CUBLAS_OP_T, CUBLAS_OP_N, na, nr, na, &one, d_Sa + (size_t)ja_best * na * na, na, d_T, na,
-                      &zero, smoothed_dev, na));
+  MC_CUDA(dgemm<false>(nr, na, nr, d_Sr + (size_t)jr_best * nr * nr, nr, 0, values_dev, na, 0, d_T, na, 0, 1, st));
+  MC_CUDA(dgemm<true>(nr, na, na, d_T, na, 0, d_Sa + (size_t)ja_best * na * na, na, 0, smoothed_dev, na, 0, 1, st));
   if (h_used_host) { h_used_host[0] = h_r[jr_best]; h_used_host[1] = h_a[ja_best]; }
   // the workspace is freed below: wait for the products that read it
   MC_CUDA(cudaStreamSynchronize(st));

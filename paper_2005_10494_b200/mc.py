@@ -60,6 +60,8 @@ def lib() -> ctypes.CDLL:
         L.mc_problem_formula10.argtypes = [i32, P(d), P(d), d, d, P(mc_problem)]; L.mc_problem_formula10.restype = i32
         L.mc_problem_strata.argtypes = [d, d, d, P(d), P(mc_problem)]; L.mc_problem_strata.restype = i32
         L.mc_fwer.argtypes = [P(mc_problem), P(d), i64, P(d), i32]; L.mc_fwer.restype = i32
+        L.mc_solve_alpha_n.argtypes = [P(mc_problem), i32, P(i32), i64, P(d), P(ctypes.c_uint8), i32]
+        L.mc_solve_alpha_n.restype = i32
         L.mc_candidates.argtypes = [P(mc_problem), i32, i32, i64, u64, P(d), P(i32), i64, P(i64), i32]
         L.mc_candidates.restype = i32
         L.mc_design_init.argtypes = [P(vp), P(mc_problem), i32, P(d), P(i32), i64, u64, i32, i32]
@@ -94,7 +96,8 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer", "mc_candidates",
+EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer",
+            "mc_solve_alpha_n", "mc_candidates",
             "mc_design_init", "mc_design_upload", "mc_set_sampling", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_evaluate_crossed", "mc_finalize_crossed", "mc_finalize", "mc_smooth_plan",
             "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_grid_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
@@ -184,6 +187,19 @@ def fwer(problem: mc_problem, alpha, device: int = 0) -> np.ndarray:
     out = np.zeros(a.shape[0])
     _check(lib().mc_fwer(ctypes.byref(problem), _dp(a), a.shape[0], _dp(out), device))
     return out
+
+
+def solve_alpha_n(problems, alpha, problem_of_design, device: int = 0):
+    """Row a1 for explicit partial designs: alpha_n solved on the GPU (Formula 2).  alpha[count, n] (the last
+    column is overwritten).  Returns (alpha with alpha_n, valid mask)."""
+    arr = _problem_array(problems)
+    n = problems[0].n
+    A = np.array(alpha, dtype=np.float64, order="C").reshape(-1, n)
+    pod = np.ascontiguousarray(problem_of_design, dtype=np.int32)
+    ok = np.zeros(len(A), dtype=np.uint8)
+    _check(lib().mc_solve_alpha_n(arr, len(problems), pod.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(A),
+                                  _dp(A), ok.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), device))
+    return A, ok.astype(bool)
 
 
 def candidates(problems, m: int = 64, n3: int = 0, seed: int = 0, device: int = 0):
@@ -496,10 +512,17 @@ def shard_range(total: int, rank: int, world: int, align: int = 64):
 
 
 def allreduce_sums(sums):
-    """Row a7: the single cross-GPU combine.  Integer SUM => bit-identical for any world size."""
+    """Row a7: the single cross-GPU combine.  Integer SUM => bit-identical for any world size.  Over NCCL
+    the device tensor is reduced in place; a gloo process group (CPU tests, bench --dist-backend gloo)
+    reduces a host copy and writes it back."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        if sums.is_cuda and dist.get_backend() == "gloo":
+            host = sums.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM)
+            sums.copy_(host)
+        else:
+            dist.all_reduce(sums, op=dist.ReduceOp.SUM)
     return sums
 
 

@@ -9,6 +9,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 SEED = 0x0000002005105494          # the arXiv id; Philox key = (lo, hi)
+FRESH_SEED = SEED ^ 0x00F1F1F100F1F1F1   # f1: fresh draws at the continuous optimum alpha* (independent key)
 ALPHA0 = 0.025                      # P:221 / P:255, one-sided 0.025 (reading R9)
 GRID_M = 64                         # candidate alpha grid per free dimension (reading R10)
 N3 = 2000                           # P:221 / P:308 "N3 = 2000 random selected values of alpha"

@@ -273,3 +273,80 @@ def test_batched_plan_matches_oracle(O, mc, torch):
             ref, _ = O.tps_smooth(x, yk, lam[k])
         assert np.allclose(sm[off:off + len(x)], ref, rtol=0, atol=1e-9), k
         off += len(x)
+
+
+def test_solve_alpha_n_explicit_points(O, mc):
+    """mc_solve_alpha_n (row a1 for explicit partial designs) against the oracle's bisection: alpha_n within
+    1e-11 and feasibility identical, for n = 2, 3 (one thread per point) and n = 4, 6 (chain CTAs)."""
+    for n in (2, 3, 4, 6):
+        spec = W.c5_problem(n)
+        prob = lib_problem(mc, spec)
+        part = np.zeros((12, n))
+        part[:, 0] = (np.arange(12) + 0.5) * spec.alpha0 / 12
+        part[:, 1:n - 1] = 0.002
+        A, ok = mc.solve_alpha_n([prob], part, np.zeros(12, dtype=np.int32))
+        for a, v in zip(A, ok):
+            ref = O.solve_alpha_n(spec.r, spec.alpha0, a[:n - 1], 1e-14)
+            assert v == (ref is not None), (n, a)
+            if v:
+                assert abs(a[-1] - ref) <= 1e-11, (n, a[-1], ref)
+                assert np.allclose(a[:n - 1], part[np.where((part[:, 0] == a[0]))[0][0], :n - 1], atol=0)
+    with pytest.raises(mc.McError):
+        mc.solve_alpha_n([lib_problem(mc, W.c2_slice())], [[0.03, 0.01, 0.0]], [0])   # alpha_1 > alpha0
+
+
+def _grid_sites(rng, count, m=64, alpha0=0.025):
+    """`count` distinct points of the half-offset m x m (alpha_1, alpha_2) grid (a seeded stand-in for the
+    N3 subset: the smoother sees only coordinates and values), alpha_3 = 0.01 (not used by a9)."""
+    g = np.sort(rng.choice(m * m, size=count, replace=False))
+    a = np.zeros((count, 3))
+    a[:, 0] = (g // m + 0.5) * alpha0 / m
+    a[:, 1] = (g % m + 0.5) * alpha0 / m
+    a[:, 2] = 0.01
+    return a
+
+
+def _c2_noise_values(rng, x):
+    """A C2-shaped surface (max ~0.977 in the interior, curvature of the slice) plus 1e6-draw MC noise."""
+    f = 0.977 - 0.02 * (x[:, 0] - 0.1) ** 2 - 0.015 * (x[:, 1] - 0.55) ** 2 + 0.004 * x[:, 0] * x[:, 1]
+    return f + 1.5e-4 * rng.normal(size=len(f))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("sizes", [(2000, 2000, 2000, 2000), (2495,)])
+def test_full_size_tps_parity(O, mc, torch, sizes):
+    """TPS + GCV at the full C2/C3 sizes against the oracle's dense definition (one solve per
+    grid lambda, numpy): four equal N = 2000 problems take the batched eigensolver (cusolverDnXsyevBatched),
+    one N = 2495 problem (the C3 slice's size) the Dsyevd lane.  GCV lambda = the oracle's first minimiser
+    over the grid window +-3 around it (or GCV scores equal to 1e-9 relative) and smoothed values within 1e-9
+    of the oracle's dense solve at that lambda."""
+    rng = np.random.default_rng(sum(sizes))
+    specs = W.c2_problems()[::97][:len(sizes)]
+    probs, alpha, pod, xs, ys = [], [], [], [], []
+    for k, (sp, N) in enumerate(zip(specs, sizes)):
+        a = _grid_sites(rng, N)
+        probs.append(lib_problem(mc, sp))
+        alpha.append(a)
+        pod += [k] * N
+        xs.append(a[:, :2] / sp.alpha0)
+        ys.append(_c2_noise_values(rng, xs[-1]))
+    dsg = mc.Design(probs, np.concatenate(alpha), np.array(pod, dtype=np.int32), seed=1)
+    sm, lam = dsg.smooth(torch.tensor(np.concatenate(ys), dtype=torch.float64, device="cuda"), -1.0)
+    sm, lam = sm.cpu().numpy(), lam.cpu().numpy()
+    grid = O.GCV_LOG10_GRID
+    off = 0
+    for k, (x, y) in enumerate(zip(xs, ys)):
+        if k in (0, len(xs) - 1):        # the oracle on the first and last problem
+            # the oracle's GCV (one dense solve per lambda, ~3 s at N = 2000) on the grid window +-3 around the
+            # GPU's pick: the pick is that window's first minimiser, or tied with it to 1e-9
+            j = int(np.argmin(np.abs(grid - np.log10(lam[k]))))
+            assert 10.0 ** grid[j] == pytest.approx(lam[k], rel=1e-12)
+            win = list(range(max(0, j - 3), min(len(grid), j + 4)))
+            g = np.array([O.gcv_score(x, y, 10.0 ** grid[i]) for i in win])
+            jo = win[int(np.argmin(g))]
+            assert jo == j or g[win.index(j)] == pytest.approx(g.min(), rel=1e-9), (k, j, jo, g)
+            ref, _, _ = O.tps_fit(x, y, float(lam[k]))
+            err = np.abs(sm[off:off + len(x)] - ref).max()
+            assert err <= 1e-9, (k, err)
+        off += len(x)
+    dsg.close()

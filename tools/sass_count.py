@@ -119,17 +119,36 @@ FP32X2_OPS = ("FFMA2", "FMUL2", "FADD2")  # packed pairs: one issue slot, two FP
 SFU_OPS = ("MUFU",)
 
 
-def pipe_mix(n: int = 3, est: int = 0, lib: str = None) -> dict:
-    """Per-draw counts of the executed common path by pipe class: issue slots, FP32 (FFMA/FMUL/FADD),
-    SFU (MUFU) and IMAD.WIDE (the Philox multiplies)."""
-    path = steady_loop(sass(n, est, lib))
-    L = draws_per_iter(n, est)
+# sm_100a per-SMSP pipe model, measured on this pool's B200 (tools/pipemix.cu + ncu pipe counters,
+# profiles/r02/pipe_model.md): cycles one warp-instruction occupies each unit.
+#   FFMA2/FMUL2/FADD2   fmaheavy 2 AND fmalite 2      FFMA/FMUL/FADD   fmaheavy 2 OR fmalite 2
+#   IMAD (32-bit)       fmaheavy 2                     IMAD.WIDE        fmaheavy 4
+#   LOP3/FMNMX/FSEL/FSETP/IADD3/MOV/SHF/...  alu 2     MUFU / F2F       xu 8
+# and one issue slot per instruction.
+ALU_OPS = ("LOP3", "FMNMX", "FMNMX3", "FSEL", "FSETP", "ISETP", "IADD3", "MOV", "SHF", "SEL", "PRMT", "LEA",
+           "VIADD", "IADD", "FLO", "POPC", "VIMNMX")
+
+
+def pipe_mix(n: int = 3, est: int = 0, lib: str = None, model: int = 0) -> dict:
+    """Per-draw counts of the executed common path by pipe class: issue slots, FP32 lane-ops (FFMA/FMUL/FADD;
+    packed x2 count twice), SFU (MUFU), IMAD.WIDE (the Philox multiplies), and the per-WARP-draw cycles of
+    each unit under the measured pipe model (scalar FP32 placed on fmalite, i.e. the fmaheavy lower bound)."""
+    path = steady_loop(sass(n, est, lib, model))
+    L = draws_per_iter(n, est) if model == 0 else 2
     ops = [(t.split()[1] if t.startswith("@") else t.split()[0]) for _, t in path]
     base = [o.split(".")[0] for o in ops]
+    p2 = sum(b in FP32X2_OPS for b in base)
+    sc = sum(b in FP32_OPS for b in base)
+    wide = sum(o.startswith("IMAD.WIDE") for o in ops)
+    imad = sum(b == "IMAD" for b in base) - wide
+    alu = sum(b in ALU_OPS for b in base)
+    xu = sum(b in SFU_OPS or b == "F2F" for b in base)
     return {"issue": len(path) / L,
-            "fp32": (sum(b in FP32_OPS for b in base) + 2 * sum(b in FP32X2_OPS for b in base)) / L,
+            "fp32": (sc + 2 * p2) / L,
             "sfu": sum(b in SFU_OPS for b in base) / L,
-            "imad_wide": sum(o.startswith("IMAD.WIDE") for o in ops) / L}
+            "imad_wide": wide / L,
+            "cycles": {"issue": len(path) / L, "fmaheavy": (2 * p2 + 4 * wide + 2 * imad) / L,
+                       "fmalite": (2 * p2 + 2 * sc) / L, "alu": 2 * alu / L, "xu": 8 * xu / L}}
 
 
 def main():
