@@ -646,8 +646,8 @@ class OracleCheck:
         self.k, self.cap = args.check_k, args.check_cap
         self.capped = len(sel) > args.check_cap
         self.sel = sel[:args.check_cap] if self.capped else sel
-        self.cores = max(1, (os.cpu_count() or 2) - 2)     # leave cores for the GPU process
-        nch = max(1, -(-4 * self.cores // len(self.sel)))  # ~4 jobs per process
+        self.cores = max(1, (os.cpu_count() or 2) - 1)     # one core stays with the GPU process
+        nch = self.cores                                    # designs x cores equal jobs: no ragged last round
         bounds = [N * k // nch for k in range(nch + 1)]
         spec = c3["spec"]
         self.jobs = [(spec.r, spec.delta0(), spec.i3, spec.alpha0, c3["alpha"][d].tolist(), c3["est"], W.SEED, d,
