@@ -41,8 +41,8 @@ from paper_2005_10494_b200 import workloads as W  # noqa: E402
 # library being timed by tools/sass_count.py under the measured pipe model (DESIGN.md §4,
 # profiles/r02/pipe_model.md).  The fallback constants are that tool's output for the committed kernel.
 PIPE_MIX_FALLBACK = {
-    "cond": {"issue": 110.5, "fp32": 79.5, "sfu": 10.0, "imad_wide": 18.0,
-             "cycles": {"issue": 110.5, "fmaheavy": 151.0, "fmalite": 82.0, "alu": 78.0, "xu": 80.0}},
+    "cond": {"issue": 98.5, "fp32": 71.5, "sfu": 10.0, "imad_wide": 13.5,
+             "cycles": {"issue": 98.5, "fmaheavy": 123.5, "fmalite": 74.0, "alu": 74.0, "xu": 80.0}},
     "ind": {"issue": 108.0, "fp32": 26.0, "sfu": 12.0, "imad_wide": 27.0,
             "cycles": {"issue": 108.0, "fmaheavy": 109.0, "fmalite": 52.0, "alu": 82.0, "xu": 96.0}}}
 

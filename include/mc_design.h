@@ -264,10 +264,11 @@ mc_status mc_argmax(mc_ctx* ctx, const double* values_dev, int64_t* idx_dev, dou
 
 int64_t mc_num_designs(const mc_ctx* ctx);
 int32_t mc_num_problems(const mc_ctx* ctx);
-/* Stream words consumed per sample: IND 2 ceil((p+n)/2); COND p + floor(n/2), since
- * COND samples come in records of two (2j, 2j+1) sharing p Box-Muller pairs (2p words) followed by
- * each sample's floor(n/2) SOV uniforms.  -1 for a null ctx. */
-int32_t mc_words_per_draw(const mc_ctx* ctx);
+/* Stream words per RECORD: COND records are sample pairs (2j, 2j+1) of U = 2p + 2 floor(n/2)
+ * uniforms (p shared Box-Muller pairs, then each sample's SOV uniforms), IND records single samples of
+ * U = 2 ceil((p+n)/2) uniforms; the U 23-bit uniforms are packed into 2 ceil(23 U / 64) words.  -1 for a
+ * null ctx. */
+int32_t mc_words_per_record(const mc_ctx* ctx);
 
 /* K3 (test hook): Philox words exactly as the kernels generate them.  out_dev[i] = word word_dev[i] of
  * the stream (id_dev[i], tag) for `seed` (lane w mod 4 of the block with counter

@@ -77,10 +77,34 @@ uint32_t or_word(uint64_t seed, uint32_t design, uint64_t w)
     return out[w % 4];
 }
 
-/* Uniforms from the low 23 bits k of a word.                */
-static double u_radius(uint32_t w) { return 1.0 - (double)(w & 0x7FFFFFu) / 8388608.0; }   /* (0,1] */
-static double u_angle(uint32_t w)  { return (double)(w & 0x7FFFFFu) / 8388608.0; }         /* [0,1) */
-static double u_open(uint32_t w)   { return ((double)(w & 0x7FFFFFu) + 0.5) / 8388608.0; } /* (0,1) */
+/* Uniforms from a 23-bit field k.                          */
+static double u_radius(uint32_t k) { return 1.0 - (double)k / 8388608.0; }   /* (0,1] */
+static double u_angle(uint32_t k)  { return (double)k / 8388608.0; }         /* [0,1) */
+static double u_open(uint32_t k)   { return ((double)k + 0.5) / 8388608.0; } /* (0,1) */
+
+/* Records (round 2): a record of U uniforms starts at word w0.  If 2 ceil(23 U / 64) < U
+ * (U >= 8) the record is PACKED into W = 2 ceil(23 U / 64) words and uniform i is the 23-bit field at bit
+ * offset 23 i of the record's bit string, in which bit b is bit (b mod 32) of word w0 + floor(b / 32);
+ * otherwise W = U and uniform i is the low 23 bits of word w0 + i.                                      */
+static int record_packed(int uniforms) { return 2 * ((23 * uniforms + 63) / 64) < uniforms; }
+
+static uint32_t record_field(uint64_t seed, uint32_t id, uint32_t tag, uint64_t w0, int U, int i)
+{
+    if (!record_packed(U)) return or_word_tagged(seed, id, tag, w0 + (uint64_t)i) & 0x7FFFFFu;
+    const uint64_t bit = 23u * (uint64_t)i;
+    const uint64_t j = bit / 32;
+    const int sh = (int)(bit % 32);
+    uint64_t v = or_word_tagged(seed, id, tag, w0 + j);
+    if (sh + 23 > 32) v |= (uint64_t)or_word_tagged(seed, id, tag, w0 + j + 1) << 32;
+    return (uint32_t)((v >> sh) & 0x7FFFFFu);
+}
+
+int or_record_words(int uniforms) { return record_packed(uniforms) ? 2 * ((23 * uniforms + 63) / 64) : uniforms; }
+
+uint32_t or_record_field(uint64_t seed, uint32_t id, uint32_t tag, uint64_t w0, int uniforms, int i)
+{
+    return record_field(seed, id, tag, w0, uniforms, i);
+}
 
 /* ------------------------------------------------------------------------- */
 /* Standard normal CDF and quantile.                                          */
@@ -179,49 +203,70 @@ void or_null_corr(int n, const double *r, double *S)
  *   est    0 = COND (Genz SOV), 1 = IND (Formula 6/7 indicator)
  * Outputs (may be NULL): eps[p] prior normals, delta[n], b[n], w_null[n] (IND) .
  * Returns u in [0,1]: the success probability (COND) or indicator (IND).    */
-int or_words_per_draw(int n, int p, int est)
+/* Uniforms per record: COND records are sample pairs (2j, 2j+1) sharing p Box-Muller pairs (2p uniforms)
+ * followed by each sample's n/2 SOV uniforms; IND records are single samples of ceil((p+n)/2) pairs.   */
+int or_record_uniforms(int n, int p, int est)
 {
-    if (est == 0) return p + n / 2;     /* a record of 2 samples takes 2p + 2(n/2) words */
+    if (est == 0) return 2 * p + 2 * (n / 2);
     return 2 * ((p + n + 1) / 2);
 }
 
-/* Box-Muller: pair j uses words 2j (radius) and 2j+1 (angle) after w0. */
-static void bm_normals(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0, int nnorm, double *normals)
+/* Box-Muller: pair j uses record uniforms 2j (radius) and 2j + 1 (angle) of the U-uniform
+ * record starting at word w0. */
+static void bm_normals_rec(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0, int U, int nnorm,
+                           double *normals)
 {
     for (int j = 0; 2 * j < nnorm; ++j) {
-        double R = sqrt(-2.0 * log(u_radius(or_word_tagged(seed, design, tag, w0 + 2 * j))));
-        double a = 2.0 * M_PI * u_angle(or_word_tagged(seed, design, tag, w0 + 2 * j + 1));
+        double R = sqrt(-2.0 * log(u_radius(record_field(seed, design, tag, w0, U, 2 * j))));
+        double a = 2.0 * M_PI * u_angle(record_field(seed, design, tag, w0, U, 2 * j + 1));
         normals[2 * j] = R * cos(a);
         normals[2 * j + 1] = R * sin(a);
     }
 }
 
-/* The normals of sample s and the word index of its first SOV uniform.
- * COND: samples come in records of two, (2j, 2j+1), of 2p + 2(n/2) words starting at word j(2p + 2(n/2)):
- * words [0, 2p) are p Box-Muller pairs giving 2p normals, sample 2j takes normals [0, p) and sample
- * 2j+1 normals [p, 2p); then sample 2j's n/2 uniforms, then sample 2j+1's.
- * IND: sample s takes words [sU, (s+1)U), U = 2 ceil((p+n)/2): p prior normals then n null normals. */
-static uint64_t sample_normals(int n, int p, int est, uint64_t seed, uint32_t design, uint32_t tag, uint64_t s,
-                               double *normals)
+/* The crossed estimator's streams (tags 2, 3) keep one uniform per word: pair j uses words w0 + 2j and
+ * w0 + 2j + 1, the 23-bit field being the word's low 23 bits.                                        */
+static void bm_normals(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0, int nnorm, double *normals)
 {
-    if (est == 1) {
-        const uint64_t w0 = s * (uint64_t)or_words_per_draw(n, p, est);
-        bm_normals(seed, design, tag, w0, p + n, normals);
-        return w0 + 2 * ((p + n + 1) / 2);
+    for (int j = 0; 2 * j < nnorm; ++j) {
+        double R = sqrt(-2.0 * log(u_radius(or_word_tagged(seed, design, tag, w0 + 2 * j) & 0x7FFFFFu)));
+        double a = 2.0 * M_PI * u_angle(or_word_tagged(seed, design, tag, w0 + 2 * j + 1) & 0x7FFFFFu);
+        normals[2 * j] = R * cos(a);
+        normals[2 * j + 1] = R * sin(a);
     }
-    const uint64_t wr = 2 * (uint64_t)p + 2 * (uint64_t)(n / 2);
-    const uint64_t w0 = (s / 2) * wr;
+}
+
+/* The normals of sample s; writes the record's first word and the record index of the sample's first
+ * SOV uniform.
+ * COND: samples come in records of two, (2j, 2j+1), record j starting at word j W (W = or_record_words of
+ * 2p + 2(n/2) uniforms): uniforms [0, 2p) are p Box-Muller pairs giving 2p normals, sample 2j takes
+ * normals [0, p) and sample 2j+1 normals [p, 2p); then sample 2j's n/2 SOV uniforms, then sample 2j+1's.
+ * IND: sample s is record s (W words of 2 ceil((p+n)/2) uniforms): p prior normals then n null normals.  */
+static void sample_normals(int n, int p, int est, uint64_t seed, uint32_t design, uint32_t tag, uint64_t s,
+                           double *normals, uint64_t *rec_w0, int *sov_u0)
+{
+    const int U = or_record_uniforms(n, p, est);
+    const uint64_t W = (uint64_t)or_record_words(U);
+    if (est == 1) {
+        *rec_w0 = s * W;
+        bm_normals_rec(seed, design, tag, *rec_w0, U, p + n, normals);
+        *sov_u0 = U;
+        return;
+    }
+    *rec_w0 = (s / 2) * W;
     const int h = (int)(s % 2);
     double rec[4 * OR_MAXN + 4];
-    bm_normals(seed, design, tag, w0, 2 * p, rec);
+    bm_normals_rec(seed, design, tag, *rec_w0, U, 2 * p, rec);
     for (int k = 0; k < p; ++k) normals[k] = rec[h * p + k];
-    return w0 + 2 * (uint64_t)p + (uint64_t)h * (n / 2);
+    *sov_u0 = 2 * p + h * (n / 2);
 }
 
 /* Utility of one draw given the thresholds b of Phi_Sigma0 (Formulas 4-7):
- * IND uses the null normals w[0..n); COND reads its uniforms at word vw0 + a. */
+ * IND uses the null normals w[0..n); COND reads its SOV uniforms at record uniforms u0 + a of the
+ * rec_u-uniform record starting at word rw0. */
 static double utility_from_b(int n, const double *r, const double *b, const double *w, int est,
-                             uint64_t seed, uint32_t design, uint32_t tag, uint64_t vw0, double *wnull_out)
+                             uint64_t seed, uint32_t design, uint32_t tag, uint64_t rw0, int rec_u, int u0,
+                             double *wnull_out)
 {
     double S0[OR_MAXN * OR_MAXN], L0[OR_MAXN * OR_MAXN];
     or_null_corr(n, r, S0);
@@ -269,7 +314,7 @@ static double utility_from_b(int n, const double *r, const double *b, const doub
         prod *= e;
         if (prod == 0.0) break;                        /* u = 1 exactly; later stages are irrelevant */
         if (a < neven) {
-            double v = u_open(or_word_tagged(seed, design, tag, vw0 + a));
+            double v = u_open(record_field(seed, design, tag, rw0, rec_u, u0 + a));
             y[a] = or_Phi_inv(v * e);
         }
     }
@@ -282,7 +327,9 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
                double *eps_out, double *delta_out, double *b_out, double *wnull_out)
 {
     double normals[2 * OR_MAXN + 2];
-    const uint64_t vw0 = sample_normals(n, p, est, seed, design, tag, s, normals);
+    uint64_t rw0;
+    int u0;
+    sample_normals(n, p, est, seed, design, tag, s, normals, &rw0, &u0);
     /* Formula 10: Delta = theta + Lp * eps. */
     double delta[OR_MAXN], b[OR_MAXN];
     for (int i = 0; i < n; ++i) {
@@ -295,7 +342,8 @@ double or_draw(int n, int p, const double *r, double i3, const double *theta, co
     if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
     if (delta_out) for (int i = 0; i < n; ++i) delta_out[i] = delta[i];
     if (b_out) for (int i = 0; i < n; ++i) b_out[i] = b[i];
-    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, vw0, wnull_out);
+    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, rw0, or_record_uniforms(n, p, est), u0,
+                          wnull_out);
 }
 
 /* C4 strata prior (a synthetic extension inside the Formula-3 model, not in the paper).
@@ -313,7 +361,9 @@ double or_draw_strata(double r2, double i3, const double *sp, const double *z, i
     const int n = 2, p = 5;
     const double r[2] = { 1.0, r2 };
     double normals[2 * OR_MAXN + 2];
-    const uint64_t vw0 = sample_normals(n, p, est, seed, design, tag, s, normals);
+    uint64_t rw0;
+    int u0;
+    sample_normals(n, p, est, seed, design, tag, s, normals, &rw0, &u0);
     const double pi = 1.0 / (1.0 + exp(-(sp[0] + sp[1] * normals[0])));
     const double dp = sp[2] + sp[3] * normals[1];
     const double dm = sp[4] + sp[5] * normals[2];
@@ -331,7 +381,8 @@ double or_draw_strata(double r2, double i3, const double *sp, const double *z, i
     if (eps_out) for (int k = 0; k < p; ++k) eps_out[k] = normals[k];
     if (delta_out) { delta_out[0] = d1; delta_out[1] = d2; }
     if (b_out) { b_out[0] = b[0]; b_out[1] = b[1]; }
-    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, vw0, wnull_out);
+    return utility_from_b(n, r, b, normals + p, est, seed, design, tag, rw0, or_record_uniforms(n, p, est), u0,
+                          wnull_out);
 }
 
 void or_design_sums_strata(double r2, double i3, const double *sp, const double *z, int est, uint64_t seed,
@@ -431,7 +482,7 @@ double or_mvn_orthant(int n, const double *r, const double *b)
     double *xs[OR_MAXN], *ws[OR_MAXN], *hv[OR_MAXN];
     double *buf = (double *)malloc(sizeof(double) * 3 * (size_t)need * (n - 1));
     if (!buf) return NAN;
-    int m[OR_MAXN];
+    int m[OR_MAXN] = { 0 };
     for (int k = 0; k + 1 < n; ++k) {
         xs[k] = buf + (size_t)need * (3 * k);
         ws[k] = xs[k] + need;

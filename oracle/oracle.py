@@ -53,7 +53,9 @@ def lib():
         L.or_threshold.argtypes = [d]; L.or_threshold.restype = d
         L.or_cholesky.argtypes = [i32, P(d), P(d)]; L.or_cholesky.restype = i32
         L.or_null_corr.argtypes = [i32, P(d), P(d)]
-        L.or_words_per_draw.argtypes = [i32, i32, i32]; L.or_words_per_draw.restype = i32
+        L.or_record_uniforms.argtypes = [i32, i32, i32]; L.or_record_uniforms.restype = i32
+        L.or_record_words.argtypes = [i32]; L.or_record_words.restype = i32
+        L.or_record_field.argtypes = [u64, u32, u32, u64, i32, i32]; L.or_record_field.restype = u32
         L.or_word_tagged.argtypes = [u64, u32, u32, u64]
         L.or_word_tagged.restype = u32
         L.or_draw.argtypes = [i32, i32, P(d), d, P(d), P(d), P(d), i32, u64, u32, u32, u64,
@@ -104,8 +106,20 @@ def word_tagged(seed: int, ident: int, tag: int, w: int) -> int:
     return int(lib().or_word_tagged(seed, ident, tag, w))
 
 
-def words_per_draw(n: int, p: int, est: int) -> int:
-    return int(lib().or_words_per_draw(n, p, est))
+def record_uniforms(n: int, p: int, est: int) -> int:
+    """Uniforms per record: COND sample pairs 2p + 2(n/2), IND single samples 2 ceil((p+n)/2)."""
+    return int(lib().or_record_uniforms(n, p, est))
+
+
+def record_words(n: int, p: int, est: int) -> int:
+    """Words per record: 2 ceil(23 U / 64) for U record uniforms when that is fewer than U (packed), else U
+    (DESIGN.md §2.2)."""
+    return int(lib().or_record_words(record_uniforms(n, p, est)))
+
+
+def record_field(seed: int, ident: int, tag: int, w0: int, uniforms: int, i: int) -> int:
+    """The 23-bit field of uniform i of the `uniforms`-uniform record starting at word w0 of stream (id, tag)."""
+    return int(lib().or_record_field(seed, ident, tag, w0, uniforms, i))
 
 
 # --------------------------------------------------------------------------------------

@@ -499,7 +499,7 @@ mc_status mc_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, 
 
 int64_t mc_num_designs(const mc_ctx* c) { return c ? c->D : -1; }
 int32_t mc_num_problems(const mc_ctx* c) { return c ? c->n_probs : -1; }
-int32_t mc_words_per_draw(const mc_ctx* c) { return c ? words_per_draw(c->n, c->est, c->model) : -1; }
+int32_t mc_words_per_record(const mc_ctx* c) { return c ? words_per_record(c->n, c->est, c->model) : -1; }
 int32_t mc_draw_dump_stride(const mc_ctx* c) { return c ? draw_dump_stride(c->n, c->est, c->model) : -1; }
 int64_t mc_kernel_launches(const mc_ctx* c) { return c ? c->launches.load() : (int64_t)-1; }
 

@@ -6,7 +6,8 @@
 //   n = 2: int_{-inf}^{z1} phi(x) Phi((z2 - rho1 x)/s1) dx
 //   n = 3: int_{-inf}^{z2} phi(x) Phi((z1 - rho1 x)/s1) Phi((z3 - rho2 x)/s2) dx   (X1 _|_ X3 | X2)
 // evaluated by composite 10-point Gauss-Legendre on [-9, min(z, 9)] with panels no wider than half
-// the narrowest conditional sigmoid, one thread per point.  n >= 4 runs the chain's forward filtering
+// the narrowest conditional sigmoid, one warp per point (node factors that do not depend on alpha_n are
+// computed once per point; k_fwer keeps one thread per point).  n >= 4 runs the chain's forward filtering
 // recursion with one CTA per point (k_chain): the densities of X_1..X_{n-1} restricted to their
 // orthant are built once per point, so each step of the alpha_n solve is one 1-D sum.
 #include <cuda_runtime.h>
@@ -237,44 +238,75 @@ __device__ uint8_t illinois_alpha_n(int n, double alpha0, double* a, FW fw) {
   return ok;
 }
 
-__device__ uint8_t solve_alpha_n_dev(const ProbChain& pc, double* a) {
-  return illinois_alpha_n(pc.ch.n, pc.alpha0, a, [&](double x) {
-    a[pc.ch.n - 1] = x;
-    return fwer_dev(a, pc.ch);
-  });
-}
-
-// One thread per (problem, grid point) of the half-offset m^(n-1) grid (n <= 3).
-__global__ void k_alpha_grid(const ProbChain* __restrict__ pcs, int32_t n_probs, int32_t m, int64_t G,
-                             double* __restrict__ A, uint8_t* __restrict__ valid) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)n_probs * G) return;
-  const int k = (int)(t / G);
-  const int64_t g = t % G;
-  const ProbChain pc = pcs[k];
+// n <= 3, one WARP per point (the candidate grid and explicit points).  The orthant is the 1-D integral
+// over x = X_1 (n = 2) or X_2 (n = 3) of orthant_1d with the same panels and nodes; during the alpha_n solve
+// only the last factor Phi((z_n - rho x)/s) changes, so the rest of each node's integrand,
+// g_i = w_i phi(x_i) [Phi((z_1 - rho_1 x_i)/s_1) for n = 3], is computed once into shared memory (up to
+// W1_CAP nodes; recomputed beyond) and every Illinois step costs one Phi per node, spread over the lanes.
+// The lane sums are combined by a xor butterfly, which leaves the same value in every lane (IEEE addition
+// commutes), so all lanes run the identical iteration.
+constexpr int W1_WARPS = 4, W1_CAP = 1024;
+template <int MODE>   // 0: grid point t of the m^(n-1) grid; 1: explicit partial point t (problem prob[t])
+__global__ void __launch_bounds__(32 * W1_WARPS) k_alpha_warp(const ProbChain* __restrict__ pcs,
+                                                               const int32_t* __restrict__ prob, int32_t m, int64_t G,
+                                                               int64_t T, double* __restrict__ A,
+                                                               uint8_t* __restrict__ valid) {
+  __shared__ double sg[W1_WARPS][W1_CAP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t t = blockIdx.x * (int64_t)W1_WARPS + wid;
+  if (t >= T) return;                                   // uniform per warp
+  const ProbChain pc = pcs[MODE == 0 ? (int)(t / G) : prob[t]];
   const int n = pc.ch.n;
   double a[MC_MAX_N];
-  int64_t rem = g;
-  for (int i = n - 2; i >= 0; --i) {
-    a[i] = ((double)(rem % m) + 0.5) * pc.alpha0 / m;
-    rem /= m;
+  if (MODE == 0) {
+    int64_t rem = t % G;
+    for (int i = n - 2; i >= 0; --i) {
+      a[i] = ((double)(rem % m) + 0.5) * pc.alpha0 / m;
+      rem /= m;
+    }
+  } else {
+    for (int i = 0; i < n; ++i) a[i] = A[t * n + i];
   }
-  const uint8_t ok = solve_alpha_n_dev(pc, a);
-  for (int i = 0; i < n; ++i) A[t * n + i] = a[i];
-  valid[t] = ok;
-}
-
-// One thread per explicit partial point (problem index, alpha_1..alpha_{n-1}): alpha_n in place (n <= 3).
-__global__ void k_alpha_points(const ProbChain* __restrict__ pcs, const int32_t* __restrict__ prob, int64_t count,
-                               double* __restrict__ A, uint8_t* __restrict__ valid) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= count) return;
-  const ProbChain pc = pcs[prob[t]];
-  const int n = pc.ch.n;
-  double a[MC_MAX_N];
-  for (int i = 0; i < n; ++i) a[i] = A[t * n + i];
-  valid[t] = solve_alpha_n_dev(pc, a);
-  A[t * n + n - 1] = a[n - 1];
+  uint8_t ok = 1;
+  if (n >= 2) {
+    const double z0 = z_of_alpha(a[0]), z1 = n == 3 ? z_of_alpha(a[1]) : 0.0;
+    const double up = fmin(n == 2 ? z0 : z1, QHI);
+    double wmin = fmin(1.0, pc.ch.sd[0] / pc.ch.rho[0]);
+    if (n == 3) wmin = fmin(wmin, pc.ch.sd[1] / pc.ch.rho[1]);
+    int P = up <= QLO ? 0 : (int)ceil((up - QLO) / (0.5 * wmin));
+    if (P > 40000) P = 40000;   // never reached in the validated range (s >= 1e-3 needs <= 36000 panels)
+    const double len = P > 0 ? (up - QLO) / P : 0.0;
+    const int nodes = 10 * P;
+    const bool stored = nodes <= W1_CAP;
+    const double rl = pc.ch.rho[n - 2], sl = pc.ch.sd[n - 2];
+    auto xnode = [&](int i) { return QLO + len * ((double)(i / 10) + 0.5 * (c_glx[i % 10] + 1.0)); };
+    auto gnode = [&](int i) {
+      const double x = xnode(i);
+      double g = 0.5 * len * c_glw[i % 10] * phi_d(x);
+      if (n == 3) g *= cond_cdf(z0, pc.ch.rho[0], pc.ch.sd[0], x);
+      return g;
+    };
+    if (stored)
+      for (int i = lane; i < nodes; i += 32) sg[wid][i] = gnode(i);
+    __syncwarp();
+    ok = illinois_alpha_n(n, pc.alpha0, a, [&](double an) {
+      const double zl = z_of_alpha(an);
+      double acc = 0.0;
+      for (int i = lane; i < nodes; i += 32) acc += (stored ? sg[wid][i] : gnode(i)) * cond_cdf(zl, rl, sl, xnode(i));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      return 1.0 - acc;
+    });
+  } else {
+    a[0] = pc.alpha0;
+  }
+  if (lane == 0) {
+    if (MODE == 0)
+      for (int i = 0; i < n; ++i) A[t * n + i] = a[i];
+    else
+      A[t * n + n - 1] = a[n - 1];
+    valid[t] = ok;
+  }
 }
 
 // n >= 4, one CTA per point, grid-strided.  MODE 0: grid point t of the m^(n-1) grid (alpha_n solved);
@@ -385,11 +417,11 @@ mc_status alpha_grid_solve(const mc_problem* probs, int32_t n_probs, int32_t m, 
   } else {
     if (n >= 4) e = launch_chain<0>(d_pcs, nullptr, m, G, T, d_A, d_v, nullptr);
     else {
-      k_alpha_grid<<<(unsigned)((T + 127) / 128), 128>>>(d_pcs, n_probs, m, G, d_A, d_v);
+      k_alpha_warp<0><<<(unsigned)((T + W1_WARPS - 1) / W1_WARPS), 32 * W1_WARPS>>>(d_pcs, nullptr, m, G, T, d_A, d_v);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
-      s = cuda_fail(e, "k_alpha_grid / k_chain");
+      s = cuda_fail(e, "k_alpha_warp / k_chain");
     } else {
       A.resize((size_t)T * n);
       valid.resize((size_t)T);
@@ -433,13 +465,14 @@ mc_status alpha_points_solve(const mc_problem* probs, int32_t n_probs, const int
   } else {
     if (n >= 4) e = launch_chain<1>(d_pcs, d_prob, 0, 1, count, d_A, d_v, nullptr);
     else {
-      k_alpha_points<<<(unsigned)((count + 127) / 128), 128>>>(d_pcs, d_prob, count, d_A, d_v);
+      k_alpha_warp<1><<<(unsigned)((count + W1_WARPS - 1) / W1_WARPS), 32 * W1_WARPS>>>(d_pcs, d_prob, 0, 1, count,
+                                                                                    d_A, d_v);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess ||
         (e = cudaMemcpy(A, d_A, sizeof(double) * count * n, cudaMemcpyDeviceToHost)) != cudaSuccess ||
         (e = cudaMemcpy(valid, d_v, count, cudaMemcpyDeviceToHost)) != cudaSuccess)
-      s = cuda_fail(e, "k_alpha_points / k_chain");
+      s = cuda_fail(e, "k_alpha_warp / k_chain");
   }
   cudaFree(d_pcs);
   cudaFree(d_prob);

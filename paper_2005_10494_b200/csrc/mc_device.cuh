@@ -15,8 +15,11 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
 // Geometry of the word stream for N populations, estimator EST (0 COND, 1 IND) and prior MODEL
 // (0: Gaussian, prior dimension P = N; 1: the C4 strata prior, P = 5, N = 2).  The stream of a design
-// is cut into RECORDS of R consecutive samples (DESIGN.md §2.3): COND R = 2 (a sample pair shares P
-// Box-Muller pairs: 2P normals, then NE SOV uniforms per sample), IND R = 1 (NPAIR pairs).
+// is cut into RECORDS of R consecutive samples (DESIGN.md §2.2-2.3): COND R = 2 (a sample pair shares P
+// Box-Muller pairs: 2P normals, then NE SOV uniforms per sample), IND R = 1 (NPAIR pairs).  A record's U
+// uniforms are 23-bit fields: PACKED into WR = 2 ceil(23 U / 64) words when that is fewer than U (uniform
+// i = bits [23 i, 23 i + 23) of the record's little-endian bit string; U >= 8), else one per word (its low
+// 23 bits).  n = 3 COND packs 8 uniforms into 6 words per sample pair: 1.5 Philox blocks instead of 2.
 template <int N, int EST, int MODEL = 0>
 struct Geo {
   static constexpr int P = MODEL == 1 ? 5 : N;
@@ -25,7 +28,9 @@ struct Geo {
   static constexpr int NO = (N + 1) / 2;     // COND: odd populations (analytic), 0-based index 2j
   static constexpr int R = (EST == 0) ? 2 : 1;                    // samples per record
   static constexpr int NPAIR = (EST == 0) ? P : (NNORM + 1) / 2;  // Box-Muller pairs per record
-  static constexpr int WR = (EST == 0) ? 2 * P + 2 * NE : 2 * NPAIR;   // words per record
+  static constexpr int U = (EST == 0) ? 2 * P + 2 * NE : 2 * NPAIR;    // 23-bit uniforms per record
+  static constexpr bool PACKED = 2 * ((23 * U + 63) / 64) < U;    // packing saves words (U >= 8)
+  static constexpr int WR = PACKED ? 2 * ((23 * U + 63) / 64) : U;   // words per record
   static constexpr int LR = 4 / cgcd(WR, 4);                      // records per Philox-aligned step
   static constexpr int L = R * LR;                                // samples per step
   static constexpr int BLOCKS = LR * WR / 4;                      // Philox blocks per step
@@ -135,6 +140,17 @@ __device__ __forceinline__ float word_to_f12(uint32_t w, uint32_t one) {
   asm("lop3.b32 %0, %1, 0x007FFFFF, %2, 0xEA;" : "=r"(r) : "r"(w), "r"(one));
   return __uint_as_float(r);
 }
+// Record uniform i as 1 + k 2^-23, k = the 23-bit field at bit offset 23 i of the record words w[] (PACKED)
+// or the low 23 bits of word i: one LOP3, plus one SHF (shift or funnel shift across two
+// words) for a packed field unless 23 i is a multiple of 32.  i is a compile-time constant at every call site (unrolled loops), so the word
+// indices and shifts fold.
+template <bool PACKED>
+__device__ __forceinline__ float unif_f12(const uint32_t* w, int i, uint32_t one) {
+  if constexpr (!PACKED) return word_to_f12(w[i], one);
+  const int b = 23 * i, j = b >> 5, sh = b & 31;
+  const uint32_t f = sh == 0 ? w[j] : (sh <= 9 ? (w[j] >> sh) : __funnelshift_r(w[j], w[j + 1], sh));
+  return word_to_f12(f, one);
+}
 __device__ __forceinline__ uint32_t one_bits_reg() {
   uint32_t r;
   asm volatile("mov.b32 %0, 0x3F800000;" : "=r"(r));
@@ -145,25 +161,42 @@ __device__ __forceinline__ uint32_t one_bits_reg() {
 // scaled normals eps / BM_K and folds BM_K into the per-problem factors (see problem_record()).
 constexpr float BM_K = 1.17741002251547469f;
 
-// The kernel's Box-Muller: returns (n0, n1) / BM_K.  sqrt(|log2 u_r|) replaces the clamp at 0 (log2 of
-// u_r <= 1 can come back ~1e-7 positive from MUFU.LG2); the angle 2 pi (u_a - 1/2) is one FFMA.
-__device__ __forceinline__ void box_muller_scaled(uint32_t wr, uint32_t wa, uint32_t one, float& n0, float& n1) {
-  const float ur = 2.0f - word_to_f12(wr, one);
+// The kernel's Box-Muller from the two uniforms as 1 + k 2^-23 (fr, fa): returns (n0, n1) / BM_K.
+// sqrt(|log2 u_r|) replaces the clamp at 0 (log2 of u_r <= 1 can come back ~1e-7 positive from
+// MUFU.LG2); the angle 2 pi (u_a - 1/2) is one FFMA.
+__device__ __forceinline__ void box_muller_f12(float fr, float fa, float& n0, float& n1) {
+  const float ur = 2.0f - fr;
   const float mr = -sqrt_approx(fabsf(lg2_approx(ur)));
-  const float x = fmaf(word_to_f12(wa, one), 6.28318530718f, -9.42477796077f);
+  const float x = fmaf(fa, 6.28318530718f, -9.42477796077f);
   n0 = mr * cos_approx(x);
   n1 = mr * sin_approx(x);
 }
+// ... from two whole words (the crossed estimator's streams keep one uniform per word)
+__device__ __forceinline__ void box_muller_scaled(uint32_t wr, uint32_t wa, uint32_t one, float& n0, float& n1) {
+  box_muller_f12(word_to_f12(wr, one), word_to_f12(wa, one), n0, n1);
+}
 
 // Upper normal tail q = Phi(-x), x >= 0, as ONE power of two: q = 2^E(m), m = min(|a|, PHI_CLAMP), E a
-// degree-11 polynomial in m that includes the -a^2 term (tools/fit_normal_tail_ex2.py: relative error
-// 3.6e-8 in exact arithmetic, 1.4e-6 in fp32 for x <= 4).  The argument arrives PRE-SCALED,
+// degree-9 polynomial in m that includes the -a^2 term (tools/fit_normal_tail_ex2.py: relative error 9.0e-7
+// in exact arithmetic, 1.8e-6 in fp32 for x <= 4).  The argument arrives PRE-SCALED,
 // a = x sqrt(log2(e)/2) (the COND record folds the factor into M, the thresholds and the stage
 // coefficients: mc_api.cu PHI_SCALE), so E ~ -a^2.  Beyond the clamp (x > 5.887) q is held at
-// q(5.887) = 2.0e-9, a change below 2^-28 that the per-draw 2^-23 fixed point absorbs; alpha = 0
-// (z = +inf, a = +inf) therefore gives u = 0 exactly.  One MUFU (EX2), no reciprocal: round 1's
+// q(5.887) = 2.0e-9 (reading R25): ten stages add at most 2.0e-8, below half the per-draw 2^-23
+// fixed-point step, so alpha = 0 (z = +inf, a = +inf) gives u = 0 exactly for every n <= 10.  One MUFU (EX2), no reciprocal: round 1's
 // Numerical-Recipes form t = 1/(1 + kappa x), q = t 2^(P(t) - a^2) needed RCP + EX2 per call.
 // Returns q and e = 1 - q (= Phi(x)) without cancellation for either sign of a.
+#ifndef MC_PHI_DEG
+#define MC_PHI_DEG 9      // 11: the degree-11 fit on m <= 5 (3.6e-8 exact), -4 % draws/s (profiles/r02/tune_pk2.jsonl)
+#endif
+#if MC_PHI_DEG == 9
+// degree 9 on m <= 5 (x <= 5.887, q(clamp) = 2.0e-9): relative error 9.0e-7 exact, 1.8e-6 fp32 (x <= 4)
+constexpr float PHI_CLAMP = 5.0f;
+#define MC_PHI_POLY(HORNER, m)                                                                              \
+  HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(                                         \
+      2.4093271849031533e-07f, m, -5.50882381484465e-06f), m, 4.659686919954287e-05f), m,                   \
+      -0.0001033207823907455f), m, -0.0013127185110967503f), m, 0.014977484435093462f), m,                   \
+      -0.08674957729065969f), m, -0.6362018435487484f), m, -1.355378895260889f), m, -0.9999986975583613f)
+#else
 constexpr float PHI_CLAMP = 5.0f;
 #define MC_PHI_POLY(HORNER, m)                                       \
   HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER( \
@@ -171,6 +204,7 @@ constexpr float PHI_CLAMP = 5.0f;
       -5.145014405324849e-05f), m, 0.0002655422273086682f), m, -0.0007692117070775829f), m,                    \
       -1.9095885481130195e-05f), m, 0.013417788461371934f), m, -0.08565676580912412f), m,                      \
       -0.6365931830340086f), m, -1.355324411309415f), m, -0.9999999477305315f)
+#endif
 __device__ __forceinline__ float horner1(float p, float x, float c) { return fmaf(p, x, c); }
 
 __device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
@@ -184,19 +218,32 @@ __device__ __forceinline__ void normal_tail(float a, float& q, float& e) {
 
 // Standard normal quantile Phi^{-1}(p) given p and its complement pc = 1 - p (both computed accurately by
 // the caller): Phi^{-1}(p) = g(t) (p - pc) with t = w/8 - 1, w = -ln(4 p pc) in [0, 16]
-// (p in [2.8e-8, 1 - 2.8e-8]), g ONE degree-14 polynomial in t (tools/fit_erfinv_w.py: relative error
-// 6.0e-8 in exact arithmetic, 9.6e-7 in fp32) — no square root, no per-coefficient selects and no branch.
+// (p in [2.8e-8, 1 - 2.8e-8]), g ONE degree-12 polynomial in t (tools/fit_erfinv_w.py: relative error
+// 1.3e-6 in exact arithmetic, 2.3e-6 in fp32) — no square root, no per-coefficient selects and no branch.
 // t = lg2(p pc) (-ln2/8) + (-ln4/8 - 1) is one FFMA after MUFU.LG2.  Beyond that range t is clamped to 1
 // (w = 16, reading R24): in the SOV this only happens when v e_k < 2.8e-8 (the upper side cannot clamp:
 // 1 - v >= 2^-24), and the resulting change of u is at most e_k on an event of probability
 // <= 2.8e-8 / e_k, i.e. a bias of at most 2.8e-8 per even stage.  Round 1 used a degree-12 polynomial
 // in sqrt(w + 2) (one MUFU.SQRT more per call) and before that a deep-tail branch (-4.8 % draws/s).
+#ifndef MC_QUANT_DEG
+#define MC_QUANT_DEG 12   // 14: relative error 6.0e-8 exact, one packed FFMA more per call
+#endif
+#if MC_QUANT_DEG == 12
+// degree 12: relative error 1.3e-6 exact, 2.3e-6 fp32
+#define MC_QUANTILE_POLY(HORNER, t)                                                                               \
+  HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(                         \
+      0.013822934060579422f, t, 0.01174856432856336f), t, -0.07083904242963865f), t, 0.0036023348788869554f), t, \
+      0.10475706180380204f), t, -0.08248599065262685f), t, 0.0347135537264593f), t, -0.01678848886490599f), t,   \
+      -0.046555255159994154f), t, 0.17713202118124255f), t, -0.45794967801334f), t, 1.995276138502238f), t,      \
+      3.7638474592654703f)
+#else
 #define MC_QUANTILE_POLY(HORNER, t)                                                                               \
   HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(HORNER(           \
       0.01019474611084561f, t, -0.012522037903250294f), t, -0.029537615373728402f), t, 0.05105979421834458f), t, \
       0.001191401517323608f), t, -0.0434556915527025f), t, 0.04556025718938638f), t, -0.05578006817451819f), t,  \
       0.059710341538845794f), t, -0.024018910794271674f), t, -0.05160295363704608f), t, 0.17794569832657112f), t, \
       -0.45756438521357723f), t, 1.9952513929012803f), t, 3.7638425973256995f)
+#endif
 constexpr float QT_A = -0.08664339756999316f;    // -ln2 / 8
 constexpr float QT_B = -1.1732867951399863f;     // -ln4 / 8 - 1
 
@@ -269,7 +316,8 @@ template <int N, int EST, int MODEL>
 __device__ __forceinline__ void record_normals(const uint32_t* w, uint32_t one, float* nrm) {
   using G = Geo<N, EST, MODEL>;
 #pragma unroll
-  for (int j = 0; j < G::NPAIR; ++j) box_muller_scaled(w[2 * j], w[2 * j + 1], one, nrm[2 * j], nrm[2 * j + 1]);
+  for (int j = 0; j < G::NPAIR; ++j)
+    box_muller_f12(unif_f12<G::PACKED>(w, 2 * j, one), unif_f12<G::PACKED>(w, 2 * j + 1, one), nrm[2 * j], nrm[2 * j + 1]);
 }
 
 // Sample h of a record: its normals start at nrm + h P (COND) and its SOV uniforms at word 2P + h NE.
@@ -307,7 +355,7 @@ __device__ __forceinline__ void shared_of_sample(const float* nrm, const uint32_
   } else {
 #pragma unroll
     for (int k = 0; k < G::NE; ++k)   // (k+1/2) 2^-23
-      sh.vu[k] = word_to_f12(w[2 * G::P + h * G::NE + k], one) - 0.99999994039535522f;
+      sh.vu[k] = unif_f12<G::PACKED>(w, 2 * G::P + h * G::NE + k, one) - 0.99999994039535522f;
   }
 }
 
@@ -530,13 +578,13 @@ __device__ __forceinline__ void record_utility_cond_x2(const uint32_t* w, uint32
   for (int j = 0; j < P; j += 2) {
     float ur[2], xa[2];
     if (j + 1 < P) {
-      up2(fma2(pk2(word_to_f12(w[2 * j], one), word_to_f12(w[2 * j + 2], one)), bc2(-1.0f), bc2(2.0f)),
+      up2(fma2(pk2(unif_f12<G::PACKED>(w, 2 * j, one), unif_f12<G::PACKED>(w, 2 * j + 2, one)), bc2(-1.0f), bc2(2.0f)),
           ur[0], ur[1]);
-      up2(fma2(pk2(word_to_f12(w[2 * j + 1], one), word_to_f12(w[2 * j + 3], one)), bc2(6.28318530718f),
+      up2(fma2(pk2(unif_f12<G::PACKED>(w, 2 * j + 1, one), unif_f12<G::PACKED>(w, 2 * j + 3, one)), bc2(6.28318530718f),
                bc2(-9.42477796077f)), xa[0], xa[1]);
     } else {
-      ur[0] = 2.0f - word_to_f12(w[2 * j], one);
-      xa[0] = fmaf(word_to_f12(w[2 * j + 1], one), 6.28318530718f, -9.42477796077f);
+      ur[0] = 2.0f - unif_f12<G::PACKED>(w, 2 * j, one);
+      xa[0] = fmaf(unif_f12<G::PACKED>(w, 2 * j + 1, one), 6.28318530718f, -9.42477796077f);
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -566,7 +614,7 @@ __device__ __forceinline__ void record_utility_cond_x2(const uint32_t* w, uint32
   f2x vu[NE > 0 ? NE : 1];
 #pragma unroll
   for (int k = 0; k < NE; ++k)   // the SOV uniforms (k+1/2) 2^-23 of both samples
-    vu[k] = add2(pk2(word_to_f12(w[2 * P + k], one), word_to_f12(w[2 * P + NE + k], one)),
+    vu[k] = add2(pk2(unif_f12<G::PACKED>(w, 2 * P + k, one), unif_f12<G::PACKED>(w, 2 * P + NE + k, one)),
                  bc2(-0.99999994039535522f));
   up2(utility_cond_x2<N>(b, vu, pr), u[0], u[1]);
   if constexpr (DBG) {
@@ -661,7 +709,7 @@ __device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, 
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < G::NE; ++k) sh.vu[k] = word_to_f12(w[2 * G::P + h * G::NE + k], one) - 0.99999994039535522f;
+        for (int k = 0; k < G::NE; ++k) sh.vu[k] = unif_f12<G::PACKED>(w, 2 * G::P + h * G::NE + k, one) - 0.99999994039535522f;
       }
     }
     u[h] = utility_of_b<N, EST, MODEL>(b, sh, pr);

@@ -102,7 +102,7 @@ mc_status launch_philox_dump(uint64_t seed, uint32_t tag, int form, const uint32
 mc_status launch_draw_dump(mc_ctx* c, const int64_t* design, const uint64_t* sample, int64_t count, float* out,
                            cudaStream_t st);
 int draw_dump_stride(int n, int est, int model);
-int words_per_draw(int n, int est, int model);
+int words_per_record(int n, int est, int model);
 mc_status launch_zc(mc_ctx* c, cudaStream_t st);
 mc_status launch_argmax(mc_ctx* c, const double* values, int64_t* idx, double* val, cudaStream_t st);
 mc_status alpha_grid_solve(const mc_problem* probs, int32_t n_probs, int32_t m, int device,

@@ -496,10 +496,11 @@ mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64
                      : launch_fused_est<1>(c, d0, dcount, B, E, st, sums);
 }
 
-int words_per_draw(int n, int est, int model) {
-  // Geo<N,EST,MODEL>::WR / R (words per sample) without instantiating every N
+int words_per_record(int n, int est, int model) {
+  // Geo<N,EST,MODEL>::WR without instantiating every N: U 23-bit uniforms in 2 ceil(23 U / 64) words
   const int p = model == 1 ? 5 : n;
-  return est == 0 ? p + n / 2 : 2 * ((p + n + 1) / 2);
+  const int U = est == 0 ? 2 * p + 2 * (n / 2) : 2 * ((p + n + 1) / 2);
+  return 2 * ((23 * U + 63) / 64);
 }
 int draw_dump_stride(int n, int est, int model) {
   const int p = model == 1 ? 5 : n;

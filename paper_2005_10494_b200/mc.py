@@ -87,7 +87,7 @@ def lib() -> ctypes.CDLL:
         L.mc_grid_smooth.argtypes = [vp, i32, i32, P(d), P(d), d, d, vp, P(d), vp]; L.mc_grid_smooth.restype = i32
         L.mc_num_designs.argtypes = [vp]; L.mc_num_designs.restype = i64
         L.mc_num_problems.argtypes = [vp]; L.mc_num_problems.restype = i32
-        L.mc_words_per_draw.argtypes = [vp]; L.mc_words_per_draw.restype = i32
+        L.mc_words_per_record.argtypes = [vp]; L.mc_words_per_record.restype = i32
         L.mc_philox_dump.argtypes = [u64, ctypes.c_uint32, i32, vp, vp, i64, vp, vp]; L.mc_philox_dump.restype = i32
         L.mc_draw_dump.argtypes = [vp, vp, vp, i64, vp, vp]; L.mc_draw_dump.restype = i32
         L.mc_draw_dump_stride.argtypes = [vp]; L.mc_draw_dump_stride.restype = i32
@@ -99,7 +99,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ["mc_information_units", "mc_threshold", "mc_problem_formula10", "mc_problem_strata", "mc_fwer",
             "mc_solve_alpha_n", "mc_candidates",
             "mc_design_init", "mc_design_upload", "mc_set_sampling", "mc_set_launch", "mc_destroy", "mc_evaluate_grid", "mc_evaluate_crossed", "mc_finalize_crossed", "mc_finalize", "mc_smooth_plan",
-            "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_grid_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_draw", "mc_philox_dump",
+            "mc_smooth", "mc_tps_fit", "mc_tps_eval", "mc_refine", "mc_surface_fit", "mc_surface_eval", "mc_surface_max", "mc_surface_destroy", "mc_grid_smooth", "mc_argmax", "mc_num_designs", "mc_num_problems", "mc_words_per_record", "mc_philox_dump",
             "mc_draw_dump", "mc_draw_dump_stride", "mc_kernel_launches", "mc_last_error", "mc_version"]
 
 
@@ -277,8 +277,8 @@ class Design:
             pass
 
     @property
-    def words_per_draw(self) -> int:
-        return int(lib().mc_words_per_draw(self._ctx))
+    def words_per_record(self) -> int:
+        return int(lib().mc_words_per_record(self._ctx))
 
     @property
     def launches(self) -> int:

@@ -175,3 +175,15 @@ def test_crossed_rejects_int64_overflow(mc, torch):
     dsg.evaluate_crossed(s, 1000, 2**16)               # fine
     assert int(s[0, 0]) > 0
     dsg.close()
+
+
+@pytest.mark.parametrize("est", [0, 1])
+def test_alpha_zero_never_rejects_n10(O, mc, torch, est):
+    """Reading R25: the kernel's normal CDF holds q at 2.0e-9 beyond x = 5.887; ten such stages stay below
+    half a 2^-23 step, so the all-zero design (z = +inf everywhere) has u = 0 exactly at n = 10 too."""
+    spec = W.c5_problem(10)
+    dsg = mc.Design([lib_problem(mc, spec)], np.zeros((1, 10)), np.zeros(1, dtype=np.int32), seed=SEED, estimator=est)
+    s = dsg.new_sums()
+    dsg.evaluate(s, 0, 200_000)
+    assert int(s[0, 0]) == 0 and int(s[0, 1]) == 0
+    dsg.close()

@@ -15,9 +15,9 @@ def _mc(O, r2, sp, alpha, est, N, design=0):
     return float(m[0]), float(v[0])
 
 
-def test_words_per_draw_c4(O):
-    assert O.words_per_draw(2, 5, 0) == 6      # per sample pair: 5 Box-Muller pairs + 2 SOV uniforms
-    assert O.words_per_draw(2, 5, 1) == 8      # 7 normals -> 4 pairs
+def test_record_sizes_c4(O):
+    assert O.record_uniforms(2, 5, 0) == 12 and O.record_words(2, 5, 0) == 10   # sample pair: 5 BM pairs + 2 SOV
+    assert O.record_uniforms(2, 5, 1) == 8 and O.record_words(2, 5, 1) == 6     # 7 normals -> 4 pairs, packed
 
 
 @pytest.mark.parametrize("est", [0, 1])

@@ -37,37 +37,62 @@ def test_word_stream_layout(O):
     assert a != b and a != c
 
 
-def test_words_per_draw(O):
-    # COND: a record of two samples takes p Box-Muller pairs (2p words) + 2 floor(n/2) SOV uniforms,
-    # i.e. p + floor(n/2) words per sample; IND: 2*ceil((p+n)/2) words per sample
-    assert O.words_per_draw(3, 3, 0) == 4
-    assert O.words_per_draw(3, 3, 1) == 6
-    assert O.words_per_draw(1, 1, 0) == 1
-    assert O.words_per_draw(2, 2, 0) == 3
-    assert O.words_per_draw(10, 10, 0) == 15
-    assert O.words_per_draw(10, 10, 1) == 20
+def test_record_sizes(O):
+    # records (round 2): COND sample pairs take 2p Box-Muller uniforms + 2 floor(n/2) SOV
+    # uniforms, IND single samples 2 ceil((p+n)/2); U uniforms of 23 bits are packed into W = 2 ceil(23 U / 64)
+    # words when that is fewer than U (U >= 8), else take one word each
+    assert O.record_uniforms(3, 3, 0) == 8 and O.record_words(3, 3, 0) == 6      # 184 bits in 6 words
+    assert O.record_uniforms(3, 3, 1) == 6 and O.record_words(3, 3, 1) == 6      # 2 ceil(138/64) = 6: unpacked
+    assert O.record_uniforms(1, 1, 0) == 2 and O.record_words(1, 1, 0) == 2
+    assert O.record_uniforms(2, 2, 0) == 6 and O.record_words(2, 2, 0) == 6
+    assert O.record_uniforms(4, 4, 0) == 12 and O.record_words(4, 4, 0) == 10
+    assert O.record_uniforms(10, 10, 0) == 30 and O.record_words(10, 10, 0) == 22
+    assert O.record_uniforms(10, 10, 1) == 20 and O.record_words(10, 10, 1) == 16
 
 
-def _bm(word_r, word_a):
-    # u_r = 1 - k 2^-23, u_a = k 2^-23 from the low 23 bits; R = sqrt(-2 ln u_r)
-    ur = 1.0 - (word_r & 0x7FFFFF) * 2.0 ** -23
-    ua = (word_a & 0x7FFFFF) * 2.0 ** -23
+def _record_bits(O, seed, d, w0, W, tag=0):
+    """The record's bit string as one Python integer: bit b is bit (b mod 32) of word w0 + b // 32."""
+    return sum(O.word_tagged(seed, d, tag, w0 + j) << (32 * j) for j in range(W))
+
+
+@pytest.mark.parametrize("U", [2, 6, 8, 12, 30])
+def test_record_fields_are_23_bit_slices(O, U):
+    # packed records (U >= 8): uniform i = bits [23 i, 23 i + 23) of the little-endian record bit string
+    # (big-int slice); unpacked (U <= 6): the low 23 bits of word i
+    seed, d = 0x2005105494, 7
+    packed = 2 * ((23 * U + 63) // 64) < U
+    W = 2 * ((23 * U + 63) // 64) if packed else U
+    for w0 in [0, 6 * 1234567, 4 * 2**32 - 2]:
+        bits = _record_bits(O, seed, d, w0, W)
+        for i in range(U):
+            ref = (bits >> (23 * i)) & 0x7FFFFF if packed else O.word_tagged(seed, d, 0, w0 + i) & 0x7FFFFF
+            assert O.record_field(seed, d, 0, w0, U, i) == ref, (U, w0, i)
+
+
+def _bm(kr, ka):
+    # DESIGN.md §2.3: u_r = 1 - k 2^-23, u_a = k 2^-23 from 23-bit fields; R = sqrt(-2 ln u_r)
+    ur = 1.0 - kr * 2.0 ** -23
+    ua = ka * 2.0 ** -23
     R = math.sqrt(-2.0 * math.log(ur))
     return R * math.cos(2 * math.pi * ua), R * math.sin(2 * math.pi * ua)
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4])
 def test_cond_record_layout(O, n):
-    # COND sample pair (2j, 2j+1) = words [jW, (j+1)W), W = 2n + 2(n/2): sample 2j takes the normals
-    # [0, n) of the record's n Box-Muller pairs, sample 2j+1 the normals [n, 2n)
+    # COND sample pair (2j, 2j+1) = record j at words [jW, (j+1)W): sample 2j takes the normals [0, n) of the
+    # record's n Box-Muller pairs (fields 2t, 2t+1), sample 2j+1 the normals [n, 2n) (DESIGN.md §2.3)
     seed, d = 0x2005105494, 11
     r = [1.0, 0.6, 0.35, 0.2][:n]
     prob = O.point_mass_problem(r, [0.0] * n, 100.0)
-    W = 2 * n + 2 * (n // 2)
+    U = 2 * n + 2 * (n // 2)
+    packed = 2 * ((23 * U + 63) // 64) < U
+    W = 2 * ((23 * U + 63) // 64) if packed else U
     for j in [0, 1, 7, 123457]:
+        bits = _record_bits(O, seed, d, j * W, W)
+        f = [((bits >> (23 * i)) if packed else (bits >> (32 * i))) & 0x7FFFFF for i in range(U)]
         z = []
         for t in range(n):
-            z.extend(_bm(O.word(seed, d, j * W + 2 * t), O.word(seed, d, j * W + 2 * t + 1)))
+            z.extend(_bm(f[2 * t], f[2 * t + 1]))
         for h in range(2):
             eps = O.draw(prob, [0.01] * n, O.EST_COND, seed, d, 2 * j + h)["eps"]
             assert np.allclose(eps, z[h * n:(h + 1) * n], rtol=1e-13, atol=1e-13)

@@ -19,11 +19,14 @@ import subprocess
 import sys
 
 LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2005_10494_b200", "libmc_design.so")
-def draws_per_iter(n: int, est: int) -> int:
-    """L = R * 4 / gcd(WR, 4) samples per Philox-aligned step (mc_device.cuh Geo): COND records are
-    sample pairs of WR = 2n + 2(n/2) words, IND records single samples of 2n words."""
+def draws_per_iter(n: int, est: int, model: int = 0) -> int:
+    """L = R * 4 / gcd(WR, 4) samples per Philox-aligned step (mc_device.cuh Geo): records of R samples
+    (COND 2, IND 1) and U 23-bit uniforms in WR = 2 ceil(23 U / 64) words if that is fewer than U, else U."""
     import math
-    R, WR = (2, 2 * n + 2 * (n // 2)) if est == 0 else (1, 2 * n)
+    p = 5 if model == 1 else n
+    R, U = (2, 2 * p + 2 * (n // 2)) if est == 0 else (1, 2 * ((p + n + 1) // 2))
+    W = 2 * ((23 * U + 63) // 64)
+    WR = W if W < U else U
     return R * (4 // math.gcd(WR, 4))
 
 
@@ -134,7 +137,7 @@ def pipe_mix(n: int = 3, est: int = 0, lib: str = None, model: int = 0) -> dict:
     packed x2 count twice), SFU (MUFU), IMAD.WIDE (the Philox multiplies), and the per-WARP-draw cycles of
     each unit under the measured pipe model (scalar FP32 placed on fmalite, i.e. the fmaheavy lower bound)."""
     path = steady_loop(sass(n, est, lib, model))
-    L = draws_per_iter(n, est) if model == 0 else 2
+    L = draws_per_iter(n, est, model)
     ops = [(t.split()[1] if t.startswith("@") else t.split()[0]) for _, t in path]
     base = [o.split(".")[0] for o in ops]
     p2 = sum(b in FP32X2_OPS for b in base)
