@@ -121,6 +121,8 @@ def parse():
     ap.add_argument("--tto-draws", type=int, default=W.DRAWS["C3"],
                     help="draws/design of the time-to-optimal-design run (C3 slice); 0 = skip")
     ap.add_argument("--no-oracle-check", action="store_true", help="skip the C3 north-star acceptance check")
+    ap.add_argument("--plan-overlap", action="store_true",
+                    help="build the C2 TPS plans on a host thread during the first MC pass (measured slower)")
     ap.add_argument("--check-k", type=int, default=16, help="acceptance check: the GPU's top-K designs ...")
     ap.add_argument("--check-cap", type=int, default=40, help="... plus every design within 5 SE, up to this many")
     return ap.parse_args()
@@ -234,10 +236,12 @@ def run_ours(args):
     design = mc.Design(problems, alpha, pod, seed=W.SEED, estimator=est, device=dev)
     if args.crn:
         design.set_sampling(True)
-    # TPS plans before the MC pass (building them on a host thread during the first pass,
-    # smooth_plan(wait=False), measured no faster: cuSOLVER's plan kernels and the fused kernel do not overlap)
+    # TPS plans before the MC pass.  Building them on a host thread during the first pass
+    # (Design.smooth_plan(wait=False), --plan-overlap; highest-priority streams) measured SLOWER: C2
+    # time-to-optimal 12.4-13.4 s against 11.9-12.3 s (profiles/r02/tto_c2.jsonl) — the eigensolver's
+    # blocks and the fused kernel compete for the same SMs.
     t1 = time.perf_counter()
-    design.smooth_plan()
+    design.smooth_plan(wait=not args.plan_overlap)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t1
     D, N = design.D, int(args.draws)
@@ -430,7 +434,9 @@ def run_ours(args):
                 "c4_optimal_design": c4, "n4_optimal_design": n4, "higher_dim_throughput": hd,
                 "paper_literal_crossed_problem": paper_crossed,
                 "clocks": clk,
-                "prep_s": {"candidates": round(t_cand, 3), "tps_plan": round(t_plan, 3)},
+                "prep_s": {"candidates": round(t_cand, 3),
+                           "tps_plan": None if args.plan_overlap else round(t_plan, 3),
+                           "tps_plan_mode": "overlapped with the first MC pass" if args.plan_overlap else "before the MC pass"},
                 "best_design_first_problem": int(out[0][0].item())}
         if args.dist_backend == "gloo" and world > 1:
             line["dry_run"] = "gloo process group, all ranks on one GPU: timing is not a measurement"
@@ -605,6 +611,15 @@ def higher_dim_throughput(args, mc, torch, dist, world, rank, dev, est, sm_count
 # CPU oracle (cpu_baseline, the C3 acceptance check and --impl reference).  The ONLY places bench.py
 # executes oracle/.
 
+def _nice_worker():
+    """Pool initializer of the background acceptance check: lowest CPU priority, so the GPU process's host
+    work (candidates, plan thread, launches) is not delayed by the oracle processes."""
+    try:
+        os.nice(19)
+    except OSError:
+        pass
+
+
 def _oracle_worker(job):
     from oracle import oracle as O
     r, delta0, i3, alpha0, a, est, seed, design, s0, N = job
@@ -646,7 +661,7 @@ class OracleCheck:
         self.k, self.cap = args.check_k, args.check_cap
         self.capped = len(sel) > args.check_cap
         self.sel = sel[:args.check_cap] if self.capped else sel
-        self.cores = max(1, (os.cpu_count() or 2) - 1)     # one core stays with the GPU process
+        self.cores = max(1, (os.cpu_count() or 3) - 2)     # two cores stay with the GPU process (+ plan thread)
         nch = self.cores                                    # designs x cores equal jobs: no ragged last round
         bounds = [N * k // nch for k in range(nch + 1)]
         spec = c3["spec"]
@@ -654,7 +669,7 @@ class OracleCheck:
                       bounds[k], bounds[k + 1] - bounds[k]) for d in self.sel for k in range(nch)]
         self.nch = nch
         self.t0 = time.perf_counter()
-        self.pool = mp.get_context("fork").Pool(self.cores)
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_nice_worker)
         self.async_res = self.pool.map_async(_oracle_worker, self.jobs, chunksize=1)
 
     def result(self):

@@ -89,6 +89,7 @@ struct mc_ctx {
   int n_plans = 0;
   // TPS coefficients of the last mc_refine (host): per problem sites, w, beta
   std::vector<std::vector<double>> tps_x, tps_w, tps_beta;
+  std::vector<std::vector<double>> tps_fitted;   // the TPS value at each fitted site: y - N lambda w
   std::vector<double> tps_lambda;
 };
 

@@ -168,8 +168,8 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
 // independent (no block barrier): each reduces its tile with 64-bit shuffles and lane 0 issues one
 // 64-bit atomicAdd pair.  Default launch: one tile per warp (a grid_blocks > 0 launch strides over the tiles).
 #ifndef MC_MIN_BLOCKS_C4
-#define MC_MIN_BLOCKS_C4 2
-#endif
+#define MC_MIN_BLOCKS_C4 4   // C4 strata kernel: 4 resident blocks/SM, -6 % kernel time vs 2 (profiles/r02/tto_c4.jsonl;
+#endif                       // round 1's time-to-optimal "anomaly" is host-side jitter: 0.42-1.45 s in both builds)
 constexpr int min_blocks(int n, int est, int model) {
   return model == 1 ? MC_MIN_BLOCKS_C4 : (n <= 3 ? (est == 0 ? MIN_BLOCKS_COND : MIN_BLOCKS_IND) : (n <= 5 ? 2 : 1));
 }

@@ -201,12 +201,13 @@ mc_status mc_refine(mc_ctx* c, const double* values, double lambda, double* alph
       const auto& w = c->tps_w[k];
       const auto& beta = c->tps_beta[k];
       const int64_t N = (int64_t)w.size();
-      // start: the fitted site with the largest P~; box: the candidate box of the sites
+      // start: the fitted site with the largest P~, from the TPS values at the sites y - N lambda w
+      // (O(N); evaluating the spline at every site would be O(N^2)); box: the candidate box of the sites
+      const auto& fv = c->tps_fitted[k];
       std::vector<double> lo(d, INFINITY), hi(d, -INFINITY), x0(d);
       double bestf = -INFINITY;
       for (int64_t i = 0; i < N; ++i) {
-        const double fi = tps_value_grad(X, w, beta, d, &X[i * d], nullptr);
-        if (fi > bestf) { bestf = fi; for (int j = 0; j < d; ++j) x0[j] = X[i * d + j]; }
+        if (fv[i] > bestf) { bestf = fv[i]; for (int j = 0; j < d; ++j) x0[j] = X[i * d + j]; }
         for (int j = 0; j < d; ++j) { lo[j] = std::min(lo[j], X[i * d + j]); hi[j] = std::max(hi[j], X[i * d + j]); }
       }
       res[k] = refine_box(X, w, beta, d, x0, lo, hi);

@@ -504,7 +504,11 @@ mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
       cusolverDnHandle_t bh = nullptr;
       cusolverDnParams_t prm = nullptr;
       mc_status s = MC_OK;
-      cudaError_t e = cudaStreamCreateWithFlags(&bst, cudaStreamNonBlocking);
+      // highest priority, as the Dsyevd lanes below: built during the MC pass (Design.smooth_plan(wait=False)),
+      // the eigensolver's latency-bound blocks are scheduled ahead of queued MC blocks
+      int prio_lo = 0, prio_hi = 0;
+      cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+      cudaError_t e = cudaStreamCreateWithPriority(&bst, cudaStreamNonBlocking, prio_hi);
       if (e != cudaSuccess) s = cuda_fail(e, "plan batch stream");
       if (s == MC_OK && (cusolverDnCreate(&bh) != CUSOLVER_STATUS_SUCCESS || cusolverDnCreateParams(&prm) != CUSOLVER_STATUS_SUCCESS)) {
         set_error("cusolverDnCreate failed");
@@ -668,6 +672,7 @@ mc_status tps_coefficients(mc_ctx* c, const double* values, double lambda, cudaS
   c->tps_x.assign(c->n_probs, {});
   c->tps_w.assign(c->n_probs, {});
   c->tps_beta.assign(c->n_probs, {});
+  c->tps_fitted.assign(c->n_probs, {});
   c->tps_lambda.assign(c->n_probs, 0.0);
   const int np = c->n_plans;
   if (np == 0) return MC_OK;
@@ -717,6 +722,8 @@ mc_status tps_coefficients(mc_ctx* c, const double* values, double lambda, cudaS
       for (int j = 0; j < d; ++j) X[i * d + j] = c->alpha[fit[i] * n + j] / a0;
     c->tps_w[k].assign(hw.begin() + off, hw.begin() + off + N);
     c->tps_lambda[k] = hl[k];
+    c->tps_fitted[k].resize(N);
+    for (int64_t i = 0; i < N; ++i) c->tps_fitted[k][i] = hy[off + i] - (double)N * hl[k] * hw[off + i];
     // normal equations T^T T beta = T^T r, r = y - N lambda w - K w
     const int m = d + 1;
     double A[4][4] = {{0}}, b[4] = {0};

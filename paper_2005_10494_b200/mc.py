@@ -208,10 +208,10 @@ def candidates(problems, m: int = 64, n3: int = 0, seed: int = 0, device: int = 
     arr = _problem_array(problems)
     n = problems[0].n
     need = ctypes.c_int64(0)
-    st = lib().mc_candidates(arr, len(problems), m, n3, seed, None, None, 0, ctypes.byref(need), device)
-    if st not in (0, 1):
-        _check(st)
-    cap = max(int(need.value), 1)
+    # capacity: at most min(grid size, N3) designs per problem, so one call solves the grid (a size query
+    # first would run the whole GPU solve twice)
+    G = m ** (n - 1)
+    cap = max(len(problems) * (min(G, n3) if n3 > 0 else G), 1)
     A = np.zeros((cap, n))
     pod = np.zeros(cap, dtype=np.int32)
     _check(lib().mc_candidates(arr, len(problems), m, n3, seed, _dp(A), pod.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
