@@ -335,9 +335,10 @@ static mc_status build_one(mc_ctx* c, PlanLane& ln, TpsPlan& pl, const std::vect
 }
 
 // ---- batched plan builder: problems with equal fitted-set sizes N share ONE cusolverDnXsyevBatched call
-// (measured 11 ms per N = 2000 matrix at batch 32 vs 28 ms with Dsyevd one by one) --------------------
+// (N = 2000: 12.5 ms per matrix at batch 32, 11.5 at 64, 9.9 at 128, 9.5 at 256 — profiles/r02/plan_batch*.jsonl —
+// vs 28 ms with Dsyevd one by one; batch 520 is rejected by cuSOLVER) --------------------------------------
 #ifndef MC_PLAN_BATCH
-#define MC_PLAN_BATCH 32       // matrices per batched eigensolver call
+#define MC_PLAN_BATCH 256      // matrices per batched eigensolver call
 #endif
 #ifndef MC_PLAN_BATCH_MIN
 #define MC_PLAN_BATCH_MIN 4    // smaller equal-size groups take the per-problem Dsyevd lanes
