@@ -86,6 +86,9 @@ __device__ __forceinline__ void finish_biased(uint32_t draws, uint32_t& a1, uint
 #ifndef MC_STEP_UNROLL
 #define MC_STEP_UNROLL 1
 #endif
+#ifndef MC_PIPELINE_PHILOX
+#define MC_PIPELINE_PHILOX 0   // 1: generate step t+1's Philox blocks while step t is evaluated
+#endif
 #ifndef MC_STEP_UNROLL_COND
 #define MC_STEP_UNROLL_COND MC_STEP_UNROLL
 #endif
@@ -108,12 +111,7 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
       const uint32_t c0r1 = hi1d ^ (uint32_t)(q >> 32) ^ rk.k0[0];
       uint32_t ql = q0;
       float cnt = 0.0f;
-#pragma unroll(EST == 0 ? kStepUnrollCond : kStepUnroll)
-      for (int st = 0; st < STEPS; ++st) {
-        uint32_t w[G::BLOCKS * 4];
-#pragma unroll
-        for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk.k1[0], rk, &w[4 * b]);
-        ql += G::BLOCKS;
+      auto eval_step = [&](const uint32_t* w) {
 #pragma unroll
         for (int r = 0; r < G::LR; ++r) {
           float u[G::R];
@@ -133,7 +131,35 @@ __device__ __forceinline__ void run_samples(uint64_t s_begin, uint64_t B, uint64
             for (int h = 0; h < G::R; ++h) accumulate_biased<EST>(u[h], a1, a2, cnt);
           }
         }
+      };
+#if MC_PIPELINE_PHILOX
+      // software-pipelined: the next step's Philox blocks (IMAD.WIDE / LOP3) are generated in the same
+      // basic block as this step's Box-Muller / normal-CDF chains, so the scheduler can interleave them
+      uint32_t wn[G::BLOCKS * 4];
+#pragma unroll
+      for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk.k1[0], rk, &wn[4 * b]);
+      ql += G::BLOCKS;
+#pragma unroll 1
+      for (int st = 0; st < STEPS - 1; ++st) {
+        uint32_t w[G::BLOCKS * 4];
+#pragma unroll
+        for (int k = 0; k < G::BLOCKS * 4; ++k) w[k] = wn[k];
+#pragma unroll
+        for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk.k1[0], rk, &wn[4 * b]);
+        ql += G::BLOCKS;
+        eval_step(w);
       }
+      eval_step(wn);
+#else
+#pragma unroll(EST == 0 ? kStepUnrollCond : kStepUnroll)
+      for (int st = 0; st < STEPS; ++st) {
+        uint32_t w[G::BLOCKS * 4];
+#pragma unroll
+        for (int b = 0; b < G::BLOCKS; ++b) philox_block_lo(ql + b, c0r1, lo1d, rk.k1[0], rk, &w[4 * b]);
+        ql += G::BLOCKS;
+        eval_step(w);
+      }
+#endif
       finish_biased<EST>(SAMPLES_PER_THREAD, a1, a2, cnt);
       if constexpr (EST == 1) a2 = a1;
       return;
