@@ -203,22 +203,23 @@ void or_null_corr(int n, const double *r, double *S)
  *   est    0 = COND (Genz SOV), 1 = IND (Formula 6/7 indicator)
  * Outputs (may be NULL): eps[p] prior normals, delta[n], b[n], w_null[n] (IND) .
  * Returns u in [0,1]: the success probability (COND) or indicator (IND).    */
-/* Uniforms per record: COND records are sample pairs (2j, 2j+1) sharing p Box-Muller pairs (2p uniforms)
- * followed by each sample's n/2 SOV uniforms; IND records are single samples of ceil((p+n)/2) pairs.   */
+/* Uniforms per record (records are sample pairs (2j, 2j+1)): COND shares p Box-Muller pairs (2p uniforms)
+ * between the two samples, followed by each sample's n/2 SOV uniforms; IND gives each sample its own
+ * ceil((p+n)/2) pairs, sample 2j's first.                                                            */
 int or_record_uniforms(int n, int p, int est)
 {
     if (est == 0) return 2 * p + 2 * (n / 2);
-    return 2 * ((p + n + 1) / 2);
+    return 4 * ((p + n + 1) / 2);
 }
 
-/* Box-Muller: pair j uses record uniforms 2j (radius) and 2j + 1 (angle) of the U-uniform
- * record starting at word w0. */
-static void bm_normals_rec(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0, int U, int nnorm,
+/* Box-Muller: pair j uses record uniforms 2(j0 + j) (radius) and 2(j0 + j) + 1 (angle) of
+ * the U-uniform record starting at word w0. */
+static void bm_normals_rec(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0, int U, int j0, int nnorm,
                            double *normals)
 {
     for (int j = 0; 2 * j < nnorm; ++j) {
-        double R = sqrt(-2.0 * log(u_radius(record_field(seed, design, tag, w0, U, 2 * j))));
-        double a = 2.0 * M_PI * u_angle(record_field(seed, design, tag, w0, U, 2 * j + 1));
+        double R = sqrt(-2.0 * log(u_radius(record_field(seed, design, tag, w0, U, 2 * (j0 + j)))));
+        double a = 2.0 * M_PI * u_angle(record_field(seed, design, tag, w0, U, 2 * (j0 + j) + 1));
         normals[2 * j] = R * cos(a);
         normals[2 * j + 1] = R * sin(a);
     }
@@ -238,25 +239,25 @@ static void bm_normals(uint64_t seed, uint32_t design, uint32_t tag, uint64_t w0
 
 /* The normals of sample s; writes the record's first word and the record index of the sample's first
  * SOV uniform.
- * COND: samples come in records of two, (2j, 2j+1), record j starting at word j W (W = or_record_words of
- * 2p + 2(n/2) uniforms): uniforms [0, 2p) are p Box-Muller pairs giving 2p normals, sample 2j takes
+ * Samples come in records of two, (2j, 2j+1), record j starting at word j W (W = or_record_words(U)).
+ * COND (U = 2p + 2(n/2)): uniforms [0, 2p) are p Box-Muller pairs giving 2p normals, sample 2j takes
  * normals [0, p) and sample 2j+1 normals [p, 2p); then sample 2j's n/2 SOV uniforms, then sample 2j+1's.
- * IND: sample s is record s (W words of 2 ceil((p+n)/2) uniforms): p prior normals then n null normals.  */
+ * IND (U = 4 ceil((p+n)/2)): sample 2j + h takes pairs [h c, (h+1) c), c = ceil((p+n)/2): p prior normals
+ * then n null normals.                                                                               */
 static void sample_normals(int n, int p, int est, uint64_t seed, uint32_t design, uint32_t tag, uint64_t s,
                            double *normals, uint64_t *rec_w0, int *sov_u0)
 {
     const int U = or_record_uniforms(n, p, est);
     const uint64_t W = (uint64_t)or_record_words(U);
+    *rec_w0 = (s / 2) * W;
+    const int h = (int)(s % 2);
     if (est == 1) {
-        *rec_w0 = s * W;
-        bm_normals_rec(seed, design, tag, *rec_w0, U, p + n, normals);
+        bm_normals_rec(seed, design, tag, *rec_w0, U, h * ((p + n + 1) / 2), p + n, normals);
         *sov_u0 = U;
         return;
     }
-    *rec_w0 = (s / 2) * W;
-    const int h = (int)(s % 2);
     double rec[4 * OR_MAXN + 4];
-    bm_normals_rec(seed, design, tag, *rec_w0, U, 2 * p, rec);
+    bm_normals_rec(seed, design, tag, *rec_w0, U, 0, 2 * p, rec);
     for (int k = 0; k < p; ++k) normals[k] = rec[h * p + k];
     *sov_u0 = 2 * p + h * (n / 2);
 }

@@ -15,8 +15,8 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
 // Geometry of the word stream for N populations, estimator EST (0 COND, 1 IND) and prior MODEL
 // (0: Gaussian, prior dimension P = N; 1: the C4 strata prior, P = 5, N = 2).  The stream of a design
-// is cut into RECORDS of R consecutive samples: COND R = 2 (a sample pair shares P
-// Box-Muller pairs: 2P normals, then NE SOV uniforms per sample), IND R = 1 (NPAIR pairs).  A record's U
+// is cut into RECORDS of R = 2 consecutive samples: COND (the pair shares P Box-Muller
+// pairs: 2P normals, then NE SOV uniforms per sample), IND (NPS pairs per sample, sample 0 first).  A record's U
 // uniforms are 23-bit fields: PACKED into WR = 2 ceil(23 U / 64) words when that is fewer than U (uniform
 // i = bits [23 i, 23 i + 23) of the record's little-endian bit string; U >= 8), else one per word (its low
 // 23 bits).  n = 3 COND packs 8 uniforms into 6 words per sample pair: 1.5 Philox blocks instead of 2.
@@ -26,8 +26,10 @@ struct Geo {
   static constexpr int NNORM = (EST == 0) ? P : P + N;          // normals per sample
   static constexpr int NE = N / 2;           // COND: even populations (sampled), 0-based index 2k+1
   static constexpr int NO = (N + 1) / 2;     // COND: odd populations (analytic), 0-based index 2j
-  static constexpr int R = (EST == 0) ? 2 : 1;                    // samples per record
-  static constexpr int NPAIR = (EST == 0) ? P : (NNORM + 1) / 2;  // Box-Muller pairs per record
+  static constexpr int R = 2;                                     // samples per record (a pair)
+  static constexpr int NPS = (NNORM + 1) / 2;                     // IND: Box-Muller pairs per sample
+  static constexpr int NPAIR = (EST == 0) ? P : 2 * NPS;          // Box-Muller pairs per record
+  static constexpr int SOFF = (EST == 0) ? P : 2 * NPS;           // sample h's normals start at h SOFF
   static constexpr int U = (EST == 0) ? 2 * P + 2 * NE : 2 * NPAIR;    // 23-bit uniforms per record
   static constexpr bool PACKED = 2 * ((23 * U + 63) / 64) < U;    // packing saves words (U >= 8)
   static constexpr int WR = PACKED ? 2 * ((23 * U + 63) / 64) : U;   // words per record
@@ -320,12 +322,13 @@ __device__ __forceinline__ void record_normals(const uint32_t* w, uint32_t one, 
     box_muller_f12(unif_f12<G::PACKED>(w, 2 * j, one), unif_f12<G::PACKED>(w, 2 * j + 1, one), nrm[2 * j], nrm[2 * j + 1]);
 }
 
-// Sample h of a record: its normals start at nrm + h P (COND) and its SOV uniforms at word 2P + h NE.
+// Sample h of a record: its normals start at nrm + h SOFF (COND: h P; IND: h 2 NPS) and its SOV uniforms
+// (COND) at record uniform 2P + h NE.
 template <int N, int EST, int MODEL>
 __device__ __forceinline__ void shared_of_sample(const float* nrm, const uint32_t* w, int h, uint32_t one,
                                                  const ProbRegs<N>& pr, const StrataRegs* sr, Shared<N, EST, MODEL>& sh) {
   using G = Geo<N, EST, MODEL>;
-  const float* e = nrm + h * G::P;
+  const float* e = nrm + h * G::SOFF;
   if constexpr (MODEL == 1) {
     static_assert(N == 2, "the C4 strata model has n = 2");
     const float zero[2] = {0.0f, 0.0f};
@@ -345,11 +348,11 @@ __device__ __forceinline__ void shared_of_sample(const float* nrm, const uint32_
   }
   if constexpr (EST == 1) {
     // Formula 6/7: the null draw X = L0 W by the Markov recursion
-    float x = nrm[G::P];
+    float x = e[G::P];
     sh.x[0] = x;
 #pragma unroll
     for (int i = 1; i < N; ++i) {
-      x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * nrm[G::P + i]);
+      x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * e[G::P + i]);
       sh.x[i] = x;
     }
   } else {
@@ -686,7 +689,7 @@ __device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, 
   for (int h = 0; h < G::R; ++h) {
     Shared<N, EST, MODEL> sh;
     float b[N];
-    const float* e = nrm + h * G::P;
+    const float* e = nrm + h * G::SOFF;
     if constexpr (MODEL == 1) {
       shared_of_sample<N, EST, MODEL>(nrm, w, h, one, pr, sr, sh);
 #pragma unroll
@@ -700,11 +703,11 @@ __device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, 
         b[i] = acc;
       }
       if constexpr (EST == 1) {
-        float x = nrm[G::P];
+        float x = e[G::P];
         sh.x[0] = x;
 #pragma unroll
         for (int i = 1; i < N; ++i) {
-          x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * nrm[G::P + i]);
+          x = fmaf(pr.rho[i - 1], x, pr.sd[i - 1] * e[G::P + i]);
           sh.x[i] = x;
         }
       } else {
@@ -718,7 +721,7 @@ __device__ __forceinline__ void record_utility(const uint32_t* w, uint32_t one, 
 #pragma unroll
       for (int k = 0; k < G::P; ++k) o[k] = e[k] * BM_K;
 #pragma unroll
-      for (int k = G::P; k < G::NNORM; ++k) o[k] = nrm[k] * BM_K;   // IND null normals (R = 1)
+      for (int k = G::P; k < G::NNORM; ++k) o[k] = e[k] * BM_K;   // IND null normals
 #pragma unroll
       for (int i = 0; i < N; ++i) o[G::NNORM + i] = b[i] / bsc[i];
       o[G::NNORM + N] = u[h];

@@ -523,10 +523,12 @@ mc_status launch_fused(mc_ctx* c, int64_t d0, int64_t dcount, uint64_t B, uint64
 }
 
 int words_per_record(int n, int est, int model) {
-  // Geo<N,EST,MODEL>::WR without instantiating every N: U 23-bit uniforms in 2 ceil(23 U / 64) words
+  // Geo<N,EST,MODEL>::WR without instantiating every N: U 23-bit uniforms in 2 ceil(23 U / 64) words if
+  // that is fewer than U, else one word each
   const int p = model == 1 ? 5 : n;
-  const int U = est == 0 ? 2 * p + 2 * (n / 2) : 2 * ((p + n + 1) / 2);
-  return 2 * ((23 * U + 63) / 64);
+  const int U = est == 0 ? 2 * p + 2 * (n / 2) : 4 * ((p + n + 1) / 2);
+  const int W = 2 * ((23 * U + 63) / 64);
+  return W < U ? W : U;
 }
 int draw_dump_stride(int n, int est, int model) {
   const int p = model == 1 ? 5 : n;

@@ -349,7 +349,7 @@ def test_c4_strata_prior_parity(O, mc, torch, est):
             pod.append(k)
     alpha = np.array(alpha)
     dsg = mc.Design(probs, alpha, np.array(pod, dtype=np.int32), seed=SEED, estimator=est)
-    assert dsg.words_per_record == (10 if est == 0 else 6)
+    assert dsg.words_per_record == (10 if est == 0 else 12)
     N = 40_000
     sums = dsg.new_sums()
     dsg.evaluate(sums, 0, N)

@@ -17,7 +17,7 @@ def _mc(O, r2, sp, alpha, est, N, design=0):
 
 def test_record_sizes_c4(O):
     assert O.record_uniforms(2, 5, 0) == 12 and O.record_words(2, 5, 0) == 10   # sample pair: 5 BM pairs + 2 SOV
-    assert O.record_uniforms(2, 5, 1) == 8 and O.record_words(2, 5, 1) == 6     # 7 normals -> 4 pairs, packed
+    assert O.record_uniforms(2, 5, 1) == 16 and O.record_words(2, 5, 1) == 12   # 7 normals -> 4 pairs per sample
 
 
 @pytest.mark.parametrize("est", [0, 1])

@@ -39,15 +39,16 @@ def test_word_stream_layout(O):
 
 def test_record_sizes(O):
     # records (round 2): COND sample pairs take 2p Box-Muller uniforms + 2 floor(n/2) SOV
-    # uniforms, IND single samples 2 ceil((p+n)/2); U uniforms of 23 bits are packed into W = 2 ceil(23 U / 64)
+    # uniforms, IND sample pairs 2 x 2 ceil((p+n)/2); U uniforms of 23 bits are packed into W = 2 ceil(23 U / 64)
     # words when that is fewer than U (U >= 8), else take one word each
     assert O.record_uniforms(3, 3, 0) == 8 and O.record_words(3, 3, 0) == 6      # 184 bits in 6 words
-    assert O.record_uniforms(3, 3, 1) == 6 and O.record_words(3, 3, 1) == 6      # 2 ceil(138/64) = 6: unpacked
+    assert O.record_uniforms(3, 3, 1) == 12 and O.record_words(3, 3, 1) == 10    # IND: 3 pairs per sample
     assert O.record_uniforms(1, 1, 0) == 2 and O.record_words(1, 1, 0) == 2
     assert O.record_uniforms(2, 2, 0) == 6 and O.record_words(2, 2, 0) == 6
     assert O.record_uniforms(4, 4, 0) == 12 and O.record_words(4, 4, 0) == 10
     assert O.record_uniforms(10, 10, 0) == 30 and O.record_words(10, 10, 0) == 22
-    assert O.record_uniforms(10, 10, 1) == 20 and O.record_words(10, 10, 1) == 16
+    assert O.record_uniforms(10, 10, 1) == 40 and O.record_words(10, 10, 1) == 30
+    assert O.record_uniforms(1, 1, 1) == 4 and O.record_words(1, 1, 1) == 4        # 2 ceil(92/64) = 4: unpacked
 
 
 def _record_bits(O, seed, d, w0, W, tag=0):
@@ -96,6 +97,30 @@ def test_cond_record_layout(O, n):
         for h in range(2):
             eps = O.draw(prob, [0.01] * n, O.EST_COND, seed, d, 2 * j + h)["eps"]
             assert np.allclose(eps, z[h * n:(h + 1) * n], rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_ind_record_layout(O, n):
+    # IND sample pair (2j, 2j+1) = record j at words [jW, (j+1)W), U = 4 c uniforms, c = ceil((p+n)/2): sample
+    # 2j + h takes Box-Muller pairs [h c, (h+1) c) of the record, its p prior normals first
+    seed, d = 0x2005105494, 5
+    r = [1.0, 0.6, 0.35][:n]
+    prob = O.point_mass_problem(r, [0.0] * n, 100.0)
+    c = (2 * n + 1) // 2
+    U = 4 * c
+    packed = 2 * ((23 * U + 63) // 64) < U
+    W = 2 * ((23 * U + 63) // 64) if packed else U
+    for j in [0, 3, 98765]:
+        bits = _record_bits(O, seed, d, j * W, W)
+        f = [((bits >> (23 * i)) if packed else (bits >> (32 * i))) & 0x7FFFFF for i in range(U)]
+        for h in range(2):
+            z = []
+            for t in range(c):
+                z.extend(_bm(f[2 * (h * c + t)], f[2 * (h * c + t) + 1]))
+            o = O.draw(prob, [0.01] * n, O.EST_IND, seed, d, 2 * j + h)
+            assert np.allclose(o["eps"], z[:n], rtol=1e-13, atol=1e-13)
+            if n == 1:
+                assert np.allclose(o["xnull"], z[n:2 * n], rtol=1e-13, atol=1e-13)
 
 
 def test_cond_pair_halves_independent(O):

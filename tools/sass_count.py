@@ -20,11 +20,11 @@ import sys
 
 LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2005_10494_b200", "libmc_design.so")
 def draws_per_iter(n: int, est: int, model: int = 0) -> int:
-    """L = R * 4 / gcd(WR, 4) samples per Philox-aligned step (mc_device.cuh Geo): records of R samples
-    (COND 2, IND 1) and U 23-bit uniforms in WR = 2 ceil(23 U / 64) words if that is fewer than U, else U."""
+    """L = R * 4 / gcd(WR, 4) samples per Philox-aligned step (mc_device.cuh Geo): records of R = 2 samples
+    and U 23-bit uniforms in WR = 2 ceil(23 U / 64) words if that is fewer than U, else U."""
     import math
     p = 5 if model == 1 else n
-    R, U = (2, 2 * p + 2 * (n // 2)) if est == 0 else (1, 2 * ((p + n + 1) // 2))
+    R, U = (2, 2 * p + 2 * (n // 2)) if est == 0 else (2, 4 * ((p + n + 1) // 2))
     W = 2 * ((23 * U + 63) // 64)
     WR = W if W < U else U
     return R * (4 // math.gcd(WR, 4))
