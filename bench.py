@@ -222,11 +222,14 @@ def run_ours(args):
 
     # ---- C3 slice first: time-to-optimal-design at 1e9 draws/design; its acceptance check then runs on the
     # host cores (oracle processes) while the rest of the bench keeps the GPU busy ----
-    tto, check = None, None
+    tto, check, check_error = None, None, None
     if args.tto_draws > 0:
         tto, c3 = time_to_optimal_design(args, mc, torch, dist, world, rank, dev, est)
         if rank == 0 and world == 1 and not args.no_oracle_check:
-            check = OracleCheck(c3, args)
+            try:
+                check = OracleCheck(c3, args)
+            except Exception as exc:
+                check_error = f"{type(exc).__name__}: {exc}"
 
     specs = c2_specs(args.problems)
     t_prep0 = time.perf_counter()
@@ -409,10 +412,18 @@ def run_ours(args):
     if not args.no_higher_dim:
         hd = higher_dim_throughput(args, mc, torch, dist, world, rank, dev, est, sm_count, fmax)
 
-    acc = check.result() if check is not None else None
+    acc = {"error": check_error} if check_error else None
+    if check is not None:
+        try:
+            acc = check.result()
+        except Exception as exc:          # the headline line must print even if the background check fails
+            acc = {"error": f"{type(exc).__name__}: {exc}"}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, specs, alpha, pod, seconds=args.cpu_seconds)
+        try:
+            cpu = cpu_baseline(args, specs, alpha, pod, seconds=args.cpu_seconds)
+        except Exception as exc:
+            cpu = {"error": f"{type(exc).__name__}: {exc}"}
     if world > 1:
         dist.barrier()
 

@@ -42,3 +42,23 @@ def test_c_program_c1_matches_oracle(tmp_path):
                        text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
+
+
+def test_ctypes_mc_problem_layout_matches_header(tmp_path):
+    """mc.py declares mc_problem by hand for ctypes: its size and every field offset must
+    equal what a C compiler lays out from include/mc_design.h."""
+    import ctypes
+    from paper_2005_10494_b200 import mc
+    fields = [f[0] for f in mc.mc_problem._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "mc_design.h"\nint main(void) {\n'
+                   '  printf("size %zu\\n", sizeof(mc_problem));\n'
+                   + "".join(f'  printf("{f} %zu\\n", offsetof(mc_problem, {f}));\n' for f in fields)
+                   + "  return 0;\n}\n")
+    cc = shutil.which("cc") or shutil.which("gcc")
+    exe = str(tmp_path / "layout")
+    subprocess.run([cc, "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", exe], check=True)
+    out = dict(line.split() for line in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.splitlines())
+    assert int(out["size"]) == ctypes.sizeof(mc.mc_problem)
+    for f in fields:
+        assert int(out[f]) == getattr(mc.mc_problem, f).offset, f
