@@ -369,11 +369,16 @@ def run_ours(args):
         roof = {"bound": "alu", "note": "CRN kernel: per-(design, sample) pipe model not derived", "frac": None}
     else:
         roof = kernel_roofline(mix, rate, sm_count, fmax)
-    roof.update({"traffic": None,
-                 "traffic_ncu": {"dram_bytes_per_launch": 507904, "draws_per_launch": 1.2e10,
-                                 "capture": "profiles/r01/ncu_fused_cond_x2_summary.txt (--problems 6)",
-                                 "note": "DRAM bytes scale with designs (zc, problem_of_design, sums), not draws: "
-                                         "~4e-5 B/draw; the kernel does no HBM work per draw"},
+    # DRAM bytes of the C2 launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu on this launch shape:
+    # profiles/r02/ncu_c2_traffic.csv): 39.3 MB read + 55.3 MB written per 1.026e12-draw launch — thresholds,
+    # problem_of_design and the sums' atomics; nothing per draw
+    c2_launch = (not args.crn) and args.problems == 0 and int(args.draws) == W.DRAWS["C2"] and world == 1
+    roof.update({"traffic": 94602752 if c2_launch else None,
+                 "traffic_ncu": {"dram_read_bytes": 39299584, "dram_write_bytes": 55303168,
+                                 "draws_per_launch": 1.026e12, "bytes_per_draw": 9.2e-5,
+                                 "capture": "profiles/r02/ncu_c2_traffic.csv (tools/time_fused.py --problems 513)",
+                                 "note": "DRAM bytes scale with designs (zc, problem_of_design, sums), not draws; "
+                                         "the bound is the fmaheavy pipe, not HBM"},
                  "kernel": ("mc_crn_kernel" if args.crn else "mc_fused_kernel") + f"<3,{0 if est == 0 else 1},0>",
                  "kernel_ms": round(kms, 3), "kernel_share_of_step": round(kms / (ms / args.steps), 4),
                  "peak_basis": "SMSPs x sm_max_mhz pipe-cycles/s of the binding unit; per-warp-draw unit cycles from "
