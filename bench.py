@@ -243,8 +243,13 @@ def run_ours(args):
     # (Design.smooth_plan(wait=False), --plan-overlap; highest-priority streams) measured SLOWER: C2
     # time-to-optimal 12.4-13.4 s against 11.9-12.3 s (profiles/r02/tto_c2.jsonl) — the eigensolver's
     # blocks and the fused kernel compete for the same SMs.
+    # Under N > 1 each rank plans and smooths the problems it owns (k mod N = rank) and one
+    # all_reduce assembles the smoothed surface, so the plan time divides by N.
     t1 = time.perf_counter()
-    design.smooth_plan(wait=not args.plan_overlap)
+    if world > 1:
+        design.smooth_plan_sharded(rank, world)
+    else:
+        design.smooth_plan(wait=not args.plan_overlap)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t1
     D, N = design.D, int(args.draws)
@@ -262,7 +267,7 @@ def run_ours(args):
             kev[i][1].record(stream)
         mc.allreduce_sums(sums)
         mean, var = design.finalize(sums, N)
-        sm, lam = design.smooth(mean, -1.0)
+        sm, lam = design.smooth_sharded(mean, -1.0, rank, world)
         idx, val, _ = design.argmax(sm, with_host=False)
         return idx, val, mean, var
 
@@ -274,7 +279,7 @@ def run_ours(args):
         out_w = step()
         if wi == 0 and not args.no_tto_c2:
             _, _, mean_w, _ = out_w
-            A_opt, v_opt, st_opt = design.refine(mean_w, -1.0)
+            A_opt, v_opt, st_opt = design.refine_sharded(mean_w, -1.0, rank, world)
             per_sc = {}
             for sc in ("a", "b", "c"):
                 ks = [k for k, sp in enumerate(specs) if sp.scenario == sc and st_opt[k] != 1]

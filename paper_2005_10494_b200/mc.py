@@ -422,6 +422,56 @@ class Design:
                                st.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _stream(stream)))
         return A, v, st
 
+    # ---- multi-GPU smoothing: each rank plans and smooths the problems it owns (problem k -> rank k mod G) ----
+    def owned_problems(self, rank: int, world: int) -> np.ndarray:
+        return np.arange(self.n_probs) % world == rank
+
+    def smooth_plan_sharded(self, rank: int, world: int, fit_mask=None, stream=None):
+        """Row a9 prep across G ranks: this rank builds the TPS plans of the problems it owns (k mod G = rank);
+        every other problem is masked out of the fit (a passthrough plan, no eigensolve).  G = 1: smooth_plan."""
+        if world <= 1:
+            return self.smooth_plan(fit_mask, stream)
+        own = self.owned_problems(rank, world)[self.pod]
+        m = own.astype(np.uint8) if fit_mask is None else (np.asarray(fit_mask, dtype=np.uint8) & own.astype(np.uint8))
+        return self.smooth_plan(m, stream)
+
+    def _combine_owned(self, t, rank: int, world: int, per_design: bool):
+        """Sum over ranks of each rank's values for the problems it owns (zeros elsewhere): exactly the
+        owner's values, on every rank (one all_reduce)."""
+        import torch.distributed as dist
+        torch = _torch()
+        own = self.owned_problems(rank, world)
+        mask = torch.from_numpy(own[self.pod] if per_design else own).to(t.device)
+        if t.dim() == 2:
+            mask = mask[:, None]
+        out = torch.where(mask, t, torch.zeros_like(t))
+        if dist.get_backend() == "gloo":
+            host = out.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM)
+            return host.to(t.device)
+        dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        return out
+
+    def smooth_sharded(self, values, lam: float = -1.0, rank: int = 0, world: int = 1, stream=None):
+        """Row a9 across G ranks (after smooth_plan_sharded): each rank smooths its own problems, one all_reduce
+        assembles every problem's smoothed values and lambda on all ranks.  G = 1: smooth."""
+        sm, lam_used = self.smooth(values, lam, stream)
+        if world <= 1:
+            return sm, lam_used
+        return self._combine_owned(sm, rank, world, True), self._combine_owned(lam_used, rank, world, False)
+
+    def refine_sharded(self, values, lam: float = -1.0, rank: int = 0, world: int = 1, stream=None):
+        """NEXT f1 across G ranks: each rank runs L-BFGS on the TPS of its own problems; the optima are
+        assembled on every rank by one all_reduce.  G = 1: refine."""
+        A, v, st = self.refine(values, lam, stream)
+        if world <= 1:
+            return A, v, st
+        torch = _torch()
+        dev = values.device
+        packed = torch.from_numpy(np.concatenate([A, v[:, None], st[:, None].astype(np.float64)], axis=1)).to(dev)
+        packed = self._combine_owned(packed, rank, world, False).cpu().numpy()
+        return packed[:, :self.n].copy(), packed[:, self.n].copy(), packed[:, self.n + 1].astype(np.int32)
+
     def argmax(self, values, with_host: bool = True, stream=None):
         """Row a10: per-problem argmax (device) and, if with_host, the overall (index, value)."""
         torch = _torch()

@@ -110,3 +110,62 @@ def test_gpu_shards_allreduce_equal_single_rank(world):
         assert np.array_equal(sums, ref.cpu().numpy()), est
         assert np.array_equal(mean, dsg.finalize(ref, 1_000_003)[0].cpu().numpy())
         dsg.close()
+
+
+def _smooth_worker(rank, world, port, q):
+    """One rank of the sharded smoothing: plans and smooths the problems k with k mod world == rank, runs
+    L-BFGS on them, and the all_reduce assembles every problem's results on all ranks."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    dsg, mean = _smooth_setup()
+    dsg.smooth_plan_sharded(rank, world)
+    sm, lam = dsg.smooth_sharded(mean, -1.0, rank, world)
+    A, v, st = dsg.refine_sharded(mean, -1.0, rank, world)
+    if rank == 0:
+        q.put((sm.cpu().numpy(), lam.cpu().numpy(), A, v, st))
+    dsg.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _smooth_setup():
+    from paper_2005_10494_b200 import mc
+    from paper_2005_10494_b200 import workloads as W
+    specs = W.c2_problems()[::60][:7]
+    probs = [mc.problem_formula10(s.r, s.delta0(), s.i3, s.alpha0) for s in specs]
+    alpha, pod = mc.candidates(probs, m=16, n3=100, seed=W.SEED)
+    dsg = mc.Design(probs, alpha, pod, seed=W.SEED)
+    sums = dsg.new_sums()
+    dsg.evaluate(sums, 0, 200_000)
+    mean, _ = dsg.finalize(sums, 200_000)
+    return dsg, mean
+
+
+@pytest.mark.gpu
+def test_sharded_smoothing_equals_single_rank():
+    """Multi-GPU smoothing: 3 gloo ranks on one GPU each plan / smooth / refine the problems
+    they own; the assembled smoothed values, lambdas and continuous optima equal one rank's (batched
+    eigensolves of different batch compositions: values within 1e-12, the maximisers within 1e-7)."""
+    ctx = tmp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    world = 3
+    port = 29700 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_smooth_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    sm, lam, A, v, st = q.get()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    dsg, mean = _smooth_setup()
+    rs, rl = dsg.smooth(mean, -1.0)
+    rA, rv, rst = dsg.refine(mean, -1.0)
+    dsg.close()
+    assert np.array_equal(lam, rl.cpu().numpy())
+    assert np.allclose(sm, rs.cpu().numpy(), rtol=0, atol=1e-12)
+    assert np.array_equal(st, rst)
+    assert np.allclose(v, rv, rtol=0, atol=1e-12)
+    # the maximiser of a flat maximum moves ~sqrt(1e-13) with 1e-13 changes of the spline: alpha within 1e-7
+    assert np.allclose(A, rA, rtol=0, atol=1e-7)
