@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -625,6 +626,30 @@ def higher_dim_throughput(args, mc, torch, dist, world, rank, dev, est, sm_count
         out["c5"][str(n)] = {"designs": int(dsg.D), "draws_per_design": N, "ms": ms, "draws_per_s": rate,
                              "roofline": kernel_roofline(mix, rate / world, sm_count, fmax) if mix else None}
         dsg.close()
+    # P:131 / P:395 (BASELINE configs[4]): at an equal budget of 4096 evaluations the midpoint tensor-grid
+    # quadrature of Formula 4 over the n-D prior loses accuracy with n, the MC error does not; and at 1e8
+    # draws the MC estimate sits on the exact value.  Exact values and quadrature errors: the oracle's
+    # golden file tests/golden/c5_quadrature.json (read, not executed).
+    try:
+        g = json.load(open(os.path.join(ROOT, "tests", "golden", "c5_quadrature.json")))
+        rows = {}
+        for row in g["rows"]:
+            n = int(row["n"])
+            spec = W.c5_problem(n)
+            prob = mc.problem_formula10(spec.r, spec.delta0(), spec.i3, spec.alpha0)
+            dsg = mc.Design([prob], np.array([row["alpha"]]), np.zeros(1, dtype=np.int32), seed=W.SEED,
+                            estimator=est, device=dev)
+            res = {}
+            for B in (int(row["nodes"]), 100_000_000):
+                r = mc.evaluate_design_objective(dsg, B, smooth=False, rank=rank, world=world)
+                m, se = r.mean.item(), math.sqrt(r.var.item() / B)
+                res[str(B)] = {"P_hat": m, "SE": se, "abs_error": abs(m - row["exact"])}
+            dsg.close()
+            rows[str(n)] = {"exact": row["exact"], "quadrature_nodes": row["nodes"],
+                            "quadrature_abs_error": row["abs_error"], "mc": res}
+        out["c5_error_vs_quadrature"] = rows
+    except Exception as exc:
+        out["c5_error_vs_quadrature"] = {"error": f"{type(exc).__name__}: {exc}"}
     return out
 
 
