@@ -169,3 +169,43 @@ def test_sharded_smoothing_equals_single_rank():
     assert np.allclose(v, rv, rtol=0, atol=1e-12)
     # the maximiser of a flat maximum moves ~sqrt(1e-13) with 1e-13 changes of the spline: alpha within 1e-7
     assert np.allclose(A, rA, rtol=0, atol=1e-7)
+
+
+def _nccl_worker(port, q):
+    """World size 1 over NCCL on the box's one GPU: the device-resident int64 sums the kernel wrote go through
+    NCCL's SUM all_reduce in place (the exchange bench.py runs at N > 1; mc.allreduce_sums is the identity at
+    world 1, so the collective is called directly here)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    from paper_2005_10494_b200 import mc
+    from paper_2005_10494_b200 import workloads as W
+    spec = W.c2_slice()
+    prob = mc.problem_formula10(spec.r, spec.delta0(), spec.i3, spec.alpha0)
+    alpha = np.array([[0.002, 0.0138, 0.0128], [0.01, 0.005, 0.0123], [0.0, 0.0, 0.025]])
+    dsg = mc.Design([prob], alpha, np.zeros(len(alpha), dtype=np.int32), seed=W.SEED)
+    sums = dsg.new_sums()
+    dsg.evaluate(sums, 0, 1_000_003)
+    before = sums.cpu().numpy().copy()
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    torch.cuda.synchronize()
+    q.put((dist.get_backend(), before, sums.cpu().numpy().copy()))
+    dsg.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_allreduce_of_kernel_sums_world1():
+    """Row a7 over NCCL: the pool gives one GPU per box, so NCCL runs at world size 1 — the
+    CUDA-produced device sums pass through an NCCL int64 SUM all_reduce unchanged.  The multi-rank exchange
+    itself is covered by the gloo tests above."""
+    ctx = tmp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    p = ctx.Process(target=_nccl_worker, args=(29800 + (os.getpid() % 1000), q))
+    p.start()
+    backend, before, after = q.get()
+    p.join(timeout=300)
+    assert p.exitcode == 0
+    assert backend == "nccl"
+    assert before[:, 0].min() > 0 and np.array_equal(before, after)
