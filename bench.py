@@ -122,8 +122,8 @@ def parse():
     ap.add_argument("--tto-draws", type=int, default=W.DRAWS["C3"],
                     help="draws/design of the time-to-optimal-design run (C3 slice); 0 = skip")
     ap.add_argument("--no-oracle-check", action="store_true", help="skip the C3 north-star acceptance check")
-    ap.add_argument("--plan-overlap", action="store_true",
-                    help="build the C2 TPS plans on a host thread during the first MC pass (measured slower)")
+    ap.add_argument("--plan-first", action="store_true",
+                    help="build the C2 TPS plans before the first MC pass instead of overlapping them with it")
     ap.add_argument("--check-k", type=int, default=16, help="acceptance check: the GPU's top-K designs ...")
     ap.add_argument("--check-cap", type=int, default=40, help="... plus every design within 5 SE, up to this many")
     return ap.parse_args()
@@ -240,18 +240,21 @@ def run_ours(args):
     design = mc.Design(problems, alpha, pod, seed=W.SEED, estimator=est, device=dev)
     if args.crn:
         design.set_sampling(True)
-    # TPS plans before the MC pass.  Building them on a host thread during the first pass
-    # (Design.smooth_plan(wait=False), --plan-overlap; highest-priority streams) measured SLOWER: C2
-    # time-to-optimal 12.4-13.4 s against 11.9-12.3 s (profiles/r02/tto_c2.jsonl) — the eigensolver's
-    # blocks and the fused kernel compete for the same SMs.
+    # TPS plans on a host thread during the first (warm-up) MC pass (Design.smooth_plan(wait=False)); the
+    # first smoothing joins them.  With the batched eigensolver this is 0.6-0.9 s faster than planning first
+    # (C2 time-to-optimal 8.5-8.8 s against 9.45-9.6 s warm, profiles/r02/tto_overlap.jsonl) — little
+    # overlap: the eigensolver is a chain of ~10^3 small latency-bound launches, some needing a third of an
+    # SM's registers, time-sliced with the fused kernel (occupancy-limited K1 builds change nothing,
+    # profiles/r02/tto_occupancy_overlap.jsonl, plan_kernel_resources.txt).  --plan-first plans before.
     # Under N > 1 each rank plans and smooths the problems it owns (k mod N = rank) and one
     # all_reduce assembles the smoothed surface, so the plan time divides by N.
     t1 = time.perf_counter()
     if world > 1:
         design.smooth_plan_sharded(rank, world)
     else:
-        design.smooth_plan(wait=not args.plan_overlap)
-    torch.cuda.synchronize()
+        design.smooth_plan(wait=args.plan_first)
+    if world > 1 or args.plan_first:
+        torch.cuda.synchronize()
     t_plan = time.perf_counter() - t1
     D, N = design.D, int(args.draws)
     b, c = mc.shard_range(N, rank, world)
@@ -457,8 +460,8 @@ def run_ours(args):
                 "paper_literal_crossed_problem": paper_crossed,
                 "clocks": clk,
                 "prep_s": {"candidates": round(t_cand, 3),
-                           "tps_plan": None if args.plan_overlap else round(t_plan, 3),
-                           "tps_plan_mode": "overlapped with the first MC pass" if args.plan_overlap else "before the MC pass"},
+                           "tps_plan": round(t_plan, 3) if args.plan_first else None,
+                           "tps_plan_mode": "before the MC pass" if args.plan_first else "overlapped with the first MC pass"},
                 "best_design_first_problem": int(out[0][0].item())}
         if args.dist_backend == "gloo" and world > 1:
             line["dry_run"] = "gloo process group, all ranks on one GPU: timing is not a measurement"
