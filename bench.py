@@ -42,10 +42,10 @@ from paper_2005_10494_b200 import workloads as W  # noqa: E402
 # library being timed by tools/sass_count.py under the measured pipe model (DESIGN.md §4,
 # profiles/r02/pipe_model.md).  The fallback constants are that tool's output for the committed kernel.
 PIPE_MIX_FALLBACK = {
-    "cond": {"issue": 98.5, "fp32": 71.5, "sfu": 10.0, "imad_wide": 13.5,
-             "cycles": {"issue": 98.5, "fmaheavy": 123.5, "fmalite": 74.0, "alu": 74.0, "xu": 80.0}},
-    "ind": {"issue": 102.5, "fp32": 26.0, "sfu": 12.0, "imad_wide": 22.5,
-            "cycles": {"issue": 102.5, "fmaheavy": 91.0, "fmalite": 52.0, "alu": 81.5, "xu": 96.0}}}
+    "cond": {"issue": 96.75, "fp32": 71.5, "sfu": 10.0, "imad_wide": 13.5,
+             "cycles": {"issue": 96.75, "fmaheavy": 123.0, "fmalite": 74.0, "alu": 71.0, "xu": 80.0}},
+    "ind": {"issue": 101.75, "fp32": 26.0, "sfu": 12.0, "imad_wide": 22.5,
+            "cycles": {"issue": 101.75, "fmaheavy": 90.0, "fmalite": 52.0, "alu": 81.0, "xu": 96.0}}}
 
 SMSP_PER_SM = 4            # one warp-instruction per SMSP per clock; every pipe unit exists once per SMSP
 WARP = 32
