@@ -246,6 +246,28 @@ def test_plan_built_during_mc_pass_is_identical(O, mc, torch):
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
 
 
+def test_batched_plan_during_mc_pass_is_identical(mc, torch):
+    """The C2 time-to-optimal path of bench.py: the BATCHED eigensolver plans (>= 4 equal-size problems, GPU
+    candidates) built on the plan thread while the MC pass runs on the same ctx give bit-identical sums,
+    smoothed values, lambdas and continuous optima to planning first."""
+    specs = W.c2_problems()[::60][:6]
+    probs = [mc.problem_formula10(s.r, s.delta0(), s.i3, s.alpha0) for s in specs]
+    alpha, pod = mc.candidates(probs, m=16, n3=100, seed=W.SEED)
+    outs = []
+    for wait in (True, False):
+        dsg = mc.Design(probs, alpha, pod, seed=W.SEED)
+        dsg.smooth_plan(wait=wait)
+        sums = dsg.new_sums()
+        dsg.evaluate(sums, 0, 2_000_000)
+        mean, _ = dsg.finalize(sums, 2_000_000)
+        sm, lam = dsg.smooth(mean, -1.0)
+        A, v, st = dsg.refine(mean, -1.0)
+        outs.append((sums.cpu().numpy(), sm.cpu().numpy(), lam.cpu().numpy(), A, v, st))
+        dsg.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
 def test_batched_plan_matches_oracle(O, mc, torch):
     """Problems with equal fitted-set sizes take the batched eigensolver (>= 4 per group): 6 C2 problems
     with an N3 = 60 oracle subset of the m = 12 grid each; smoothed values and GCV lambda per problem against
