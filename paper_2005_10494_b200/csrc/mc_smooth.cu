@@ -335,10 +335,16 @@ static mc_status build_one(mc_ctx* c, PlanLane& ln, TpsPlan& pl, const std::vect
 }
 
 // ---- batched plan builder: problems with equal fitted-set sizes N share ONE cusolverDnXsyevBatched call
-// (N = 2000: 12.5 ms per matrix at batch 32, 11.5 at 64, 9.9 at 128, 9.5 at 256 — profiles/r02/plan_batch*.jsonl —
-// vs 28 ms with Dsyevd one by one; batch 520 is rejected by cuSOLVER) --------------------------------------
+// (N = 2000: 12.5 ms per matrix at batch 32, 11.5 at 64, 9.9 at 128, 9.5 at 171 — profiles/r02/plan_batch*.jsonl —
+// vs 28 ms with Dsyevd one by one).  cuSOLVER 12.9's XsyevBatched rejects large batches with INVALID_VALUE
+// (m = 1997: 171 matrices accepted, 192 rejected — profiles/r02/plan_batch_limit.jsonl), so a batch holds at
+// most MC_PLAN_BATCH matrices AND at most MC_PLAN_BATCH_ELEMS matrix elements (B m^2; 171 x 1997^2 = 6.8e8),
+// and a batch whose workspace query is still rejected is split in halves and retried. ----------------------
 #ifndef MC_PLAN_BATCH
 #define MC_PLAN_BATCH 256      // matrices per batched eigensolver call
+#endif
+#ifndef MC_PLAN_BATCH_ELEMS
+#define MC_PLAN_BATCH_ELEMS 680000000LL
 #endif
 #ifndef MC_PLAN_BATCH_MIN
 #define MC_PLAN_BATCH_MIN 4    // smaller equal-size groups take the per-problem Dsyevd lanes
@@ -496,7 +502,9 @@ mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
     for (auto& kv : by_n) {
       const auto& ks = kv.second;
       if ((int)ks.size() < MC_PLAN_BATCH_MIN) { rest.insert(rest.end(), ks.begin(), ks.end()); continue; }
-      const size_t nb = (ks.size() + MC_PLAN_BATCH - 1) / MC_PLAN_BATCH, per = (ks.size() + nb - 1) / nb;
+      const int64_t mm = kv.first - d - 1;
+      const size_t cap = (size_t)std::max<int64_t>(1, std::min<int64_t>(MC_PLAN_BATCH, MC_PLAN_BATCH_ELEMS / (mm * mm)));
+      const size_t nb = (ks.size() + cap - 1) / cap, per = (ks.size() + nb - 1) / nb;
       for (size_t i = 0; i < ks.size(); i += per)
         batches.emplace_back(ks.begin() + i, ks.begin() + std::min(ks.size(), i + per));
     }
@@ -525,9 +533,23 @@ mc_status smooth_plan(mc_ctx* c, const uint8_t* mask, cudaStream_t st) {
         const int64_t N = (int64_t)fits[batches[i][0]].size(), B = (int64_t)batches[i].size();
         if (N != cur_N || B > cur_B) {
           bs.reset(new BatchScratch());
-          s = alloc_batch_scratch(*bs, bh, prm, N, d, std::max<int64_t>(B, N == bN ? bB : B));
+          const int64_t want = std::max<int64_t>(B, N == bN ? bB : B);
+          s = alloc_batch_scratch(*bs, bh, prm, N, d, want);
+          if (s != MC_OK && B > 1) {
+            // the eigensolver rejected this batch size: split the batch in halves and retry (scratch for B/2)
+            bs.reset();
+            cudaGetLastError();
+            std::vector<int> lo(batches[i].begin(), batches[i].begin() + B / 2), hi(batches[i].begin() + B / 2, batches[i].end());
+            batches[i] = lo;
+            batches.insert(batches.begin() + i + 1, hi);
+            bB = std::min<int64_t>(bB, (int64_t)hi.size());
+            cur_N = cur_B = -1;
+            s = MC_OK;
+            --i;
+            continue;
+          }
           cur_N = N;
-          cur_B = std::max<int64_t>(B, N == bN ? bB : B);
+          cur_B = want;
           if (s != MC_OK) break;
         }
         s = build_batch(c, batches[i], fits, bst, bh, prm, *bs);

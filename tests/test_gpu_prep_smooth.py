@@ -268,6 +268,30 @@ def test_batched_plan_during_mc_pass_is_identical(mc, torch):
         assert np.array_equal(a, b)
 
 
+def test_plan_beyond_the_eigensolver_batch_limit(mc, torch):
+    """256 equal-size C2 problems (one rank's share of C2 at 2 GPUs): more matrices than cusolverDnXsyevBatched
+    accepts in one call at N = 2000 (171 accepted, 192 rejected), so the plan splits them by the element cap;
+    smoothed values and lambdas equal those of the same problems planned alone (per-problem Dsyevd)."""
+    specs = W.c2_problems()[1::2][:256]
+    probs = [mc.problem_formula10(s.r, s.delta0(), s.i3, s.alpha0) for s in specs]
+    alpha, pod = mc.candidates(probs, m=W.GRID_M, n3=W.N3, seed=W.SEED)
+    dsg = mc.Design(probs, alpha, pod, seed=W.SEED)
+    rng = np.random.default_rng(4)
+    x = alpha[:, :2] / 0.025
+    y = torch.tensor(0.9 + 0.05 * np.sin(3 * x[:, 0] + x[:, 1]) + 1e-3 * rng.normal(size=len(x)), device="cuda")
+    sm, lam = dsg.smooth(y, -1.0)
+    sm, lam = sm.cpu().numpy(), lam.cpu().numpy()
+    dsg.close()
+    begin = np.searchsorted(pod, np.arange(len(probs) + 1))
+    for k in (0, 170, 255):
+        sl = slice(begin[k], begin[k + 1])
+        one = mc.Design([probs[k]], alpha[sl], np.zeros(begin[k + 1] - begin[k], dtype=np.int32), seed=W.SEED)
+        s1, l1 = one.smooth(y[sl].contiguous(), -1.0)
+        one.close()
+        assert lam[k] == pytest.approx(float(l1.cpu()[0]), rel=1e-9), k
+        assert np.allclose(sm[sl], s1.cpu().numpy(), rtol=0, atol=1e-9), k
+
+
 def test_batched_plan_matches_oracle(O, mc, torch):
     """Problems with equal fitted-set sizes take the batched eigensolver (>= 4 per group): 6 C2 problems
     with an N3 = 60 oracle subset of the m = 12 grid each; smoothed values and GCV lambda per problem against
