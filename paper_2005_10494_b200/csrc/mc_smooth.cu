@@ -338,13 +338,13 @@ static mc_status build_one(mc_ctx* c, PlanLane& ln, TpsPlan& pl, const std::vect
 // (N = 2000: 12.5 ms per matrix at batch 32, 11.5 at 64, 9.9 at 128, 9.5 at 171 — profiles/r02/plan_batch*.jsonl —
 // vs 28 ms with Dsyevd one by one).  cuSOLVER 12.9's XsyevBatched rejects large batches with INVALID_VALUE
 // (m = 1997: 171 matrices accepted, 192 rejected — profiles/r02/plan_batch_limit.jsonl), so a batch holds at
-// most MC_PLAN_BATCH matrices AND at most MC_PLAN_BATCH_ELEMS matrix elements (B m^2; 171 x 1997^2 = 6.8e8),
+// most MC_PLAN_BATCH matrices AND at most MC_PLAN_BATCH_ELEMS matrix elements (B m^2),
 // and a batch whose workspace query is still rejected is split in halves and retried. ----------------------
 #ifndef MC_PLAN_BATCH
 #define MC_PLAN_BATCH 256      // matrices per batched eigensolver call
 #endif
 #ifndef MC_PLAN_BATCH_ELEMS
-#define MC_PLAN_BATCH_ELEMS 680000000LL
+#define MC_PLAN_BATCH_ELEMS 682000000LL   // 171 x 1997^2 = 6.82e8 accepted (C2 single GPU: 3 batches of 171)
 #endif
 #ifndef MC_PLAN_BATCH_MIN
 #define MC_PLAN_BATCH_MIN 4    // smaller equal-size groups take the per-problem Dsyevd lanes
