@@ -460,8 +460,10 @@ def run_ours(args):
                 "paper_literal_crossed_problem": paper_crossed,
                 "clocks": clk,
                 "prep_s": {"candidates": round(t_cand, 3),
-                           "tps_plan": round(t_plan, 3) if args.plan_first else None,
-                           "tps_plan_mode": "before the MC pass" if args.plan_first else "overlapped with the first MC pass"},
+                           "tps_plan": round(t_plan, 3) if (args.plan_first or world > 1) else None,
+                           "tps_plan_mode": ("sharded by problem, before the MC pass" if world > 1 else
+                                             "before the MC pass" if args.plan_first else
+                                             "overlapped with the first MC pass")},
                 "best_design_first_problem": int(out[0][0].item())}
         if args.dist_backend == "gloo" and world > 1:
             line["dry_run"] = "gloo process group, all ranks on one GPU: timing is not a measurement"
